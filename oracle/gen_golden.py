@@ -1,0 +1,401 @@
+"""Generate tests/golden/*.npz by running the UNMODIFIED reference in this container.
+
+TEST INFRASTRUCTURE ONLY.  Requires /root/reference (read-only) importable as
+``ladlasso``; it does not exist on the GPU box, so the fixtures are committed
+and the tests read only the .npz files.
+
+    python oracle/gen_golden.py [--procs 8]
+
+Every fixture stores the exact input bytes and the reference's outputs
+(beta, objective, iterations, objective_evals, converged) plus the work
+counters D (ccd_descend calls) and S (coordinate steps) obtained by wrapping
+``ladlasso.locus.ccd_descend``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import itertools
+import math
+import os
+import sys
+import time
+from multiprocessing import Pool
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(os.path.dirname(HERE), "tests", "golden")
+sys.path.insert(0, HERE)
+import configs_np  # noqa: E402
+
+
+def _ref():
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import ladlasso  # noqa: F401
+
+    return ladlasso
+
+
+def _task(args):
+    kind, payload = args
+    L = _ref()
+    from ladlasso.model import Coefficients, Dataset, ProblemSpec
+
+    x, y, lam = payload["x"], payload["y"], payload["lam"]
+    spec = ProblemSpec(Dataset(x, y), lam)
+    if kind == "ccd":
+        from ladlasso.ccd import CcdConfig, ccd_descend
+
+        trace = []
+        r = ccd_descend(spec, Coefficients(payload["start"]),
+                        CcdConfig(frozen_axis=payload["frozen"], sweep_tolerance=payload["tol"],
+                                  max_sweeps=payload["sweeps"]), trace=trace)
+        return dict(beta=r.beta.beta.copy(), objective=r.objective, iterations=r.iterations,
+                    objective_evals=r.objective_evals, converged=r.converged, trace_len=len(trace),
+                    trace_monotone=bool(np.all(np.diff(np.array(trace)) <= 0)) if len(trace) > 1 else True)
+    if kind == "locus":
+        import ladlasso.locus as LL
+        from ladlasso.ccd import CcdConfig
+        from ladlasso.errors import UnboundedDirectionError
+        from ladlasso.linesearch import Bracket
+
+        counts = {"D": 0, "S": 0}
+        orig = LL.ccd_descend
+
+        def counted(spec_, start, cfg=None, trace=None):
+            res = orig(spec_, start, cfg, trace)
+            counts["D"] += 1
+            counts["S"] += res.objective_evals
+            return res
+
+        LL.ccd_descend = counted
+        try:
+            kw = dict(payload.get("cfg", {}))
+            inner = CcdConfig(sweep_tolerance=kw.pop("inner_tol", 1e-10), max_sweeps=kw.pop("inner_sweeps", 500))
+            br = kw.pop("bracket", None)
+            cfg = LL.LocusConfig(inner=inner, initial_bracket=Bracket(*br) if br is not None else None, **kw)
+            t0 = time.perf_counter()
+            try:
+                r = LL.solve_locus(spec, cfg)
+            except UnboundedDirectionError:
+                return dict(status=1, D=counts["D"], S=counts["S"])
+            wall = time.perf_counter() - t0
+        finally:
+            LL.ccd_descend = orig
+        return dict(beta=r.beta.beta.copy(), objective=r.objective, iterations=r.iterations,
+                    objective_evals=r.objective_evals, converged=r.converged, status=0,
+                    D=counts["D"], S=counts["S"], wall=wall)
+    if kind == "brute":
+        from ladlasso.brute import solve_brute
+        from ladlasso.errors import ProblemTooLargeError
+
+        try:
+            r = solve_brute(spec, **payload.get("caps", {}))
+        except ProblemTooLargeError:
+            return dict(status=2)
+        return dict(beta=r.beta.beta.copy(), objective=r.objective, vertices=r.iterations, status=0)
+    raise ValueError(kind)
+
+
+def _stack(results, d):
+    out = {}
+    B = len(results)
+    out["beta"] = np.array([r.get("beta", np.full(d, np.nan)) for r in results]).reshape(B, d)
+    for key in ("objective", "wall"):
+        if any(key in r for r in results):
+            out[key] = np.array([r.get(key, np.nan) for r in results], dtype=np.float64)
+    for key in ("iterations", "objective_evals", "status", "D", "S", "vertices", "trace_len"):
+        if any(key in r for r in results):
+            out[key] = np.array([r.get(key, -1) for r in results], dtype=np.int64)
+    for key in ("converged", "trace_monotone"):
+        if any(key in r for r in results):
+            out[key] = np.array([bool(r.get(key, False)) for r in results])
+    return out
+
+
+def _run(pool, kind, payloads, d):
+    res = pool.map(_task, [(kind, p) for p in payloads], chunksize=1)
+    return _stack(res, d)
+
+
+def gen_kat(pool):
+    L = _ref()
+    from ladlasso.fixtures import CCD_STALL_LAMBDA, ccd_stall_problem
+    from ladlasso.linesearch import PiecewiseLinear1D, weighted_median_min
+    from ladlasso.rng import Pcg32
+
+    out = {}
+    # PCG32 golden (test_datagen.py:19-24) and a longer stream for the fan seeds
+    g42 = Pcg32(42, stream=54)
+    out["pcg32_seed42"] = np.array([g42._next_u32() for _ in range(200)], dtype=np.uint32)
+    fans = [Pcg32(0x5EED + a) for a in range(8)]
+    out["pcg32_fan"] = np.array([[g._next_u32() for _ in range(64)] for g in fans], dtype=np.uint32)
+    # weighted-median KATs (test_linesearch.py:33-54) + random cases with ties
+    med_loc, med_w, med_t, med_v = [], [], [], []
+    rng = np.random.default_rng(1234)
+    cases = [([3.0], [0.7]), ([1.0, 2.0, 9.0], [1.0, 1.0, 1.0]), ([0.0, 5.0], [10.0, 1.0]),
+             ([0.0, 1.0], [1.0, 1.0])]
+    for _ in range(300):
+        n = int(rng.integers(1, 33))
+        loc = np.round(rng.standard_normal(n) * 3, int(rng.integers(0, 3)))  # rounding -> exact ties
+        w = rng.uniform(0.1, 2.0, n)
+        if rng.random() < 0.3:
+            w = np.round(w * 4) / 4 + 0.25  # dyadic weights -> exact half-sum ties
+        cases.append((loc.tolist(), w.tolist()))
+    for loc, w in cases:
+        g = PiecewiseLinear1D(np.array(loc), np.array(w), 0.0)
+        t, v = weighted_median_min(g)
+        med_loc.append(np.pad(np.array(loc, float), (0, 33 - len(loc)), constant_values=np.nan))
+        med_w.append(np.pad(np.array(w, float), (0, 33 - len(w)), constant_values=np.nan))
+        med_t.append(t)
+        med_v.append(v)
+    out["median_loc"] = np.array(med_loc)
+    out["median_w"] = np.array(med_w)
+    out["median_t"] = np.array(med_t)
+    out["median_v"] = np.array(med_v)
+    # ccd._median_location on the same cases (total = cum[-1])
+    from ladlasso.ccd import _median_location
+
+    out["median_loc_ccd"] = np.array([_median_location(np.array(l, float), np.array(w, float)) for l, w in cases])
+    # stall fixture (fixtures.py:15-20)
+    spec = ccd_stall_problem()
+    out["stall_x"] = spec.data.x.copy()
+    out["stall_y"] = spec.data.y.copy()
+    out["stall_lam"] = np.array(CCD_STALL_LAMBDA)
+    # linear-system KATs (test_brute.py:17-38) + random systems
+    from ladlasso.brute import solve_linear_system
+
+    A, Bv, S, ok = [], [], [], []
+    for _ in range(200):
+        n = int(rng.integers(1, 7))
+        a = rng.uniform(-2, 2, (n, n))
+        if rng.random() < 0.15:
+            a[int(rng.integers(0, n))] = 0.0
+        if rng.random() < 0.15 and n > 1:
+            a[1] = a[0] * 2.0
+        b = rng.uniform(-2, 2, n)
+        s = solve_linear_system(a, b)
+        A.append(np.pad(a, ((0, 6 - n), (0, 6 - n)), constant_values=np.nan))
+        Bv.append(np.pad(b, (0, 6 - n), constant_values=np.nan))
+        S.append(np.pad(s if s is not None else np.full(n, np.nan), (0, 6 - n), constant_values=np.nan))
+        ok.append(s is not None)
+    out["ls_a"], out["ls_b"], out["ls_sol"], out["ls_ok"] = np.array(A), np.array(Bv), np.array(S), np.array(ok)
+    np.savez_compressed(os.path.join(GOLDEN, "kat.npz"), **out)
+    print("kat.npz", flush=True)
+
+
+def gen_ccd(pool):
+    rng = np.random.default_rng(4321)
+    payloads = []
+    for i in range(240):
+        m = int(rng.integers(2, 32))
+        d = int(rng.integers(1, 9))
+        x = rng.standard_normal((m, d))
+        if i % 5 == 0:  # sparse columns exercise the zero-row path (ccd.py:167-169, :178-179)
+            x[rng.random((m, d)) < 0.3] = 0.0
+        y = rng.standard_normal(m) * 3
+        lam = float(rng.choice([0.0, 0.01, 0.1, 1.0, 5.0]))
+        start = rng.standard_normal(d) * (rng.random() < 0.6)
+        frozen = int(rng.integers(-1, d))
+        payloads.append(dict(x=x, y=y, lam=lam, start=start, frozen=None if frozen < 0 else frozen,
+                             tol=float(rng.choice([1e-10, 1e-7])), sweeps=int(rng.choice([500, 40, 3, 1]))))
+    # orthogonal-columns KAT (test_ccd.py:22-36)
+    payloads.append(dict(x=np.diag([1.0, -2.0, 0.5]), y=np.array([3.0, 4.0, -1.0]), lam=0.05,
+                         start=np.zeros(3), frozen=None, tol=1e-10, sweeps=500))
+    res = pool.map(_task, [("ccd", p) for p in payloads], chunksize=4)
+    B = len(payloads)
+    Mx, Dx = 32, 8
+    X = np.full((B, Mx, Dx), np.nan)
+    Y = np.full((B, Mx), np.nan)
+    out = dict(m=np.array([p["x"].shape[0] for p in payloads]), d=np.array([p["x"].shape[1] for p in payloads]),
+               lam=np.array([p["lam"] for p in payloads]),
+               frozen=np.array([-1 if p["frozen"] is None else p["frozen"] for p in payloads]),
+               tol=np.array([p["tol"] for p in payloads]), sweeps=np.array([p["sweeps"] for p in payloads]))
+    S0 = np.full((B, Dx), np.nan)
+    for k, p in enumerate(payloads):
+        m, d = p["x"].shape
+        X[k, :m, :d] = p["x"]
+        Y[k, :m] = p["y"]
+        S0[k, :d] = p["start"]
+    beta = np.full((B, Dx), np.nan)
+    for k, r in enumerate(res):
+        beta[k, : len(r["beta"])] = r["beta"]
+    out.update(x=X, y=Y, start=S0, beta=beta, objective=np.array([r["objective"] for r in res]),
+               iterations=np.array([r["iterations"] for r in res]),
+               objective_evals=np.array([r["objective_evals"] for r in res]),
+               converged=np.array([r["converged"] for r in res]),
+               trace_len=np.array([r["trace_len"] for r in res]),
+               trace_monotone=np.array([r["trace_monotone"] for r in res]))
+    np.savez_compressed(os.path.join(GOLDEN, "ccd_cases.npz"), **out)
+    print("ccd_cases.npz", flush=True)
+
+
+def gen_acceptance(pool):
+    """The reference's 200-instance oracle sweep (test_acceptance.py:96-137)."""
+    _ref()
+    from ladlasso.datagen import GenSpec, generate
+
+    grid = list(itertools.product((1, 2, 3), range(4, 13), (0.01, 0.1, 1.0)))
+    probs = []
+    for i in range(200):
+        d, m, lam = grid[i % len(grid)]
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.2, seed=9000 + i))
+        probs.append(dict(x=data.x.copy(), y=data.y.copy(), lam=lam))
+    out = {}
+    Mx, Dx = 12, 3
+    B = len(probs)
+    X = np.full((B, Mx, Dx), np.nan)
+    Y = np.full((B, Mx), np.nan)
+    for k, p in enumerate(probs):
+        m, d = p["x"].shape
+        X[k, :m, :d] = p["x"]
+        Y[k, :m] = p["y"]
+    out["x"], out["y"] = X, Y
+    out["m"] = np.array([p["x"].shape[0] for p in probs])
+    out["d"] = np.array([p["x"].shape[1] for p in probs])
+    out["lam"] = np.array([p["lam"] for p in probs])
+    for tag, cfg in (("ternary", dict(outer_search="ternary")), ("quadrature", dict(outer_search="quadrature"))):
+        r = pool.map(_task, [("locus", dict(p, cfg=cfg)) for p in probs], chunksize=2)
+        beta = np.full((B, Dx), np.nan)
+        for k, rr in enumerate(r):
+            beta[k, : len(rr["beta"])] = rr["beta"]
+        st = _stack([dict(rr, beta=np.zeros(1)) for rr in r], 1)
+        for key, v in st.items():
+            if key != "beta":
+                out[f"{tag}_{key}"] = v
+        out[f"{tag}_beta"] = beta
+    r = pool.map(_task, [("brute", p) for p in probs], chunksize=4)
+    beta = np.full((B, Dx), np.nan)
+    for k, rr in enumerate(r):
+        beta[k, : len(rr["beta"])] = rr["beta"]
+    out["brute_beta"] = beta
+    out["brute_objective"] = np.array([rr["objective"] for rr in r])
+    out["brute_vertices"] = np.array([rr["vertices"] for rr in r])
+    np.savez_compressed(os.path.join(GOLDEN, "acceptance.npz"), **out)
+    print("acceptance.npz", flush=True)
+
+
+def gen_params(pool):
+    """LocusConfig knobs: outer_axis, initial_bracket, probes, round caps, inner caps."""
+    _ref()
+    from ladlasso.datagen import GenSpec, generate
+
+    rng = np.random.default_rng(777)
+    probs, cfgs = [], []
+    for i in range(48):
+        d = 1 + i % 4
+        m = 5 + i % 8
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.2, seed=7000 + i))
+        c = dict(outer_search=("ternary", "quadrature")[i % 2])
+        k = i % 6
+        if k == 1:
+            c["outer_axis"] = int(rng.integers(0, d))
+        elif k == 2:
+            c["bracket"] = (-0.5, 0.25)
+        elif k == 3:
+            c["outer_probes"] = 4
+            c["outer_tolerance"] = 1e-6
+        elif k == 4:
+            c["outer_max_iterations"] = 5
+        elif k == 5:
+            c["inner_sweeps"] = 2
+            c["inner_tol"] = 1e-12
+        probs.append(dict(x=data.x.copy(), y=data.y.copy(), lam=(0.01, 0.1, 1.0)[i % 3], cfg=c))
+        cfgs.append(c)
+    r = pool.map(_task, [("locus", p) for p in probs], chunksize=2)
+    B, Mx, Dx = len(probs), 12, 4
+    X = np.full((B, Mx, Dx), np.nan)
+    Y = np.full((B, Mx), np.nan)
+    beta = np.full((B, Dx), np.nan)
+    for k, p in enumerate(probs):
+        m, d = p["x"].shape
+        X[k, :m, :d] = p["x"]
+        Y[k, :m] = p["y"]
+        beta[k, :d] = r[k]["beta"]
+    st = _stack([dict(rr, beta=np.zeros(1)) for rr in r], 1)
+    out = dict(x=X, y=Y, m=np.array([p["x"].shape[0] for p in probs]), d=np.array([p["x"].shape[1] for p in probs]),
+               lam=np.array([p["lam"] for p in probs]), beta=beta,
+               outer_search=np.array([0 if c["outer_search"] == "ternary" else 1 for c in cfgs]),
+               outer_axis=np.array([c.get("outer_axis", -1) for c in cfgs]),
+               has_bracket=np.array([1 if "bracket" in c else 0 for c in cfgs]),
+               bracket=np.array([c.get("bracket", (0.0, 0.0)) for c in cfgs], dtype=float),
+               outer_probes=np.array([c.get("outer_probes", 8) for c in cfgs]),
+               outer_tolerance=np.array([c.get("outer_tolerance", 1e-9) for c in cfgs]),
+               outer_max_iterations=np.array([c.get("outer_max_iterations", 200) for c in cfgs]),
+               inner_sweeps=np.array([c.get("inner_sweeps", 500) for c in cfgs]),
+               inner_tol=np.array([c.get("inner_tol", 1e-10) for c in cfgs]))
+    for key, v in st.items():
+        if key != "beta":
+            out[key] = v
+    np.savez_compressed(os.path.join(GOLDEN, "params.npz"), **out)
+    print("params.npz", flush=True)
+
+
+def _locus_fixture(pool, name, X, Y, lam, variants, brute_idx=(), extra=None):
+    B, n, p = X.shape
+    out = dict(x=X, y=Y, lam=np.broadcast_to(np.asarray(lam, float), (B,)).copy())
+    if extra:
+        out.update(extra)
+    for v in variants:
+        t0 = time.time()
+        payloads = [dict(x=X[b], y=Y[b], lam=float(out["lam"][b]), cfg=dict(outer_search=v)) for b in range(B)]
+        st = _run(pool, "locus", payloads, p)
+        for key, val in st.items():
+            out[f"{v}_{key}"] = val
+        print(f"  {name} {v}: {B} solves in {time.time() - t0:.1f}s", flush=True)
+    if len(brute_idx):
+        payloads = [dict(x=X[b], y=Y[b], lam=float(out["lam"][b])) for b in brute_idx]
+        st = _run(pool, "brute", payloads, p)
+        out["brute_idx"] = np.asarray(brute_idx)
+        for key, val in st.items():
+            out[f"brute_{key}"] = val
+    np.savez_compressed(os.path.join(GOLDEN, f"{name}.npz"), **out)
+    print(f"{name}.npz", flush=True)
+
+
+def gen_configs(pool, quick=False):
+    rng = np.random.default_rng(15649)
+    X, Y, bt = configs_np.cfg0(rng, 32 if quick else 256)
+    _locus_fixture(pool, "cfg0", X, Y, 1.0, ("ternary", "quadrature"), brute_idx=range(2 if quick else 8),
+                   extra=dict(beta_true=bt))
+    rng = np.random.default_rng(15650)
+    X, Y, lam = configs_np.cfg1(rng, 64 if quick else 512)
+    _locus_fixture(pool, "cfg1", X, Y, lam, ("ternary", "quadrature"), brute_idx=range(X.shape[0]))
+    rng = np.random.default_rng(15651)
+    X0, Y0, _ = configs_np.cfg0(rng, 8)
+    Xr = np.repeat(X0, 16, axis=0)
+    Yr = np.repeat(Y0, 16, axis=0)
+    lam = np.tile(configs_np.LAMBDA_GRID, 8)
+    _locus_fixture(pool, "cfg2", Xr, Yr, lam, ("ternary", "quadrature"), brute_idx=(0, 15))
+    rng = np.random.default_rng(15652)
+    Xd, Yd, _ = configs_np.cfg0(rng, 1)
+    total = math.comb(30, 25)
+    ks = np.unique(np.concatenate([np.arange(8), np.linspace(0, total - 1, 40).astype(np.int64)]))
+    Xs, Ys = configs_np.cfg3_subsets(Xd[0], Yd[0], ks)
+    _locus_fixture(pool, "cfg3", Xs, Ys, 0.5, ("quadrature",), brute_idx=(0, 1),
+                   extra=dict(dataset_x=Xd[0], dataset_y=Yd[0], subset_index=ks))
+    rng = np.random.default_rng(15653)
+    X, Y, bt = configs_np.cfg4(rng, 8 if quick else 32)
+    _locus_fixture(pool, "cfg4", X, Y, 1.0, ("ternary",), extra=dict(beta_true=bt))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--procs", type=int, default=os.cpu_count())
+    ap.add_argument("--only", default="")
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    os.makedirs(GOLDEN, exist_ok=True)
+    only = set(a.only.split(",")) if a.only else None
+    with Pool(a.procs) as pool:
+        for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
+                         ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick))):
+            if only is None or name in only:
+                fn(pool)
+
+
+if __name__ == "__main__":
+    main()
