@@ -1,0 +1,119 @@
+/*
+ * ladlasso_b200.h -- C ABI of the B200-native batched LAD-LASSO solver.
+ *
+ * The reference (arxiv/paper_2510_15649, /root/reference/pkg/src/ladlasso) is
+ * a pure-Python package with no FFI; its drop-in boundary is the Python
+ * function API.  Each entry point below replaces one reference function,
+ * batched over B independent problems (B, n, p) and cited file:line:
+ *
+ *   lad_locus_solve_f64     <- locus.solve_locus(spec, cfg)        locus.py:300-409
+ *   lad_locus_solve_host_f64   same, host buffers (H2D + solve + D2H inside)
+ *   lad_ccd_descend_f64     <- ccd.ccd_descend(spec, start, cfg)   ccd.py:126-206
+ *   lad_brute_solve_f64     <- brute.solve_brute(spec, ...)        brute.py:106-145
+ *   lad_objective_f64       <- model.evaluate_objective(spec, b)   model.py:151-154
+ *   lad_generate_f64        <- (no reference counterpart) device-side generation
+ *                              of the BASELINE.json config problems
+ *
+ * Conventions: device pointers unless the name says _host; calls are
+ * asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ * default stream); return 0 on success or a negative LAD_E_* code, with the
+ * message available from lad_last_error() (thread-local).  Per-problem failures
+ * never abort a batch; they are reported in `status`:
+ *   0 ok, 1 unbounded direction (UnboundedDirectionError, linesearch.py:266),
+ *   2 invalid input (InvalidInputError: non-finite data or lambda < 0).
+ * Non-convergence is not an error (converged = 0), as in the reference.
+ */
+#ifndef LADLASSO_B200_H
+#define LADLASSO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAD_OK 0
+#define LAD_E_INVALID (-1)     /* bad shape / argument (InvalidInputError) */
+#define LAD_E_TOO_LARGE (-2)   /* brute caps exceeded (ProblemTooLargeError, brute.py:66-81) */
+#define LAD_E_CUDA (-3)        /* CUDA runtime failure */
+#define LAD_E_UNSUPPORTED (-4) /* n > 32 or p > 8 */
+
+#define LAD_OUTER_TERNARY 0
+#define LAD_OUTER_QUADRATURE 1
+
+/* LocusConfig + CcdConfig + ProblemSpec.lambda_floor (locus.py:52-58, ccd.py:55-59, model.py:27). */
+typedef struct lad_locus_params {
+    int32_t outer_axis;           /* -1 = None: scan every axis in influence order */
+    int32_t outer_search;         /* LAD_OUTER_TERNARY | LAD_OUTER_QUADRATURE */
+    double outer_tolerance;       /* 1e-9 */
+    int32_t outer_probes;         /* 8 (quadrature) */
+    int32_t outer_max_iterations; /* 200 */
+    int32_t has_bracket;          /* initial_bracket given? */
+    double bracket_lo, bracket_hi;
+    double inner_sweep_tol;       /* 1e-10 */
+    int32_t inner_max_sweeps;     /* 500 */
+    double lambda_floor;          /* 1e-9 */
+} lad_locus_params;
+
+/* Per-problem outputs (SolveResult fields, model.py:113-133, plus work counters). */
+typedef struct lad_locus_out {
+    double *beta;             /* (B, p) */
+    double *objective;        /* (B,) fresh evaluate_objective(beta) */
+    int32_t *iterations;      /* locus: outer rounds; descent: sweeps */
+    int32_t *objective_evals; /* locus: curve evaluations; descent: coordinate steps */
+    uint8_t *converged;       /* (B,) */
+    uint8_t *status;          /* (B,) see above */
+    int32_t *descents;        /* (B,) ccd_descend calls (may be NULL) */
+    int64_t *steps;           /* (B,) exact coordinate steps (may be NULL) */
+} lad_locus_out;
+
+int lad_version(void);
+const char *lad_last_error(void);
+/* fills the defaults of LocusConfig()/CcdConfig() */
+void lad_default_params(lad_locus_params *prm);
+
+/* Batched solve_locus.  X (Bd, n, p), Y (Bd, n); lam (B,) raw lambdas;
+ * data_index (B,) maps problem -> dataset row (NULL = identity, Bd = B). */
+int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index, int64_t B,
+                        int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+
+/* Same with HOST pointers for inputs and outputs (pinned or pageable); the
+ * host<->device copies run inside the call on `stream`, which is synchronized
+ * before returning.  out fields are host pointers. */
+int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                             const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+
+/* Batched ccd_descend from `start` (B, p); frozen (B,) axis or -1 (NULL = none). */
+int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                        const double *start, const int32_t *frozen, double sweep_tolerance, int32_t max_sweeps,
+                        double lambda_floor, const lad_locus_out *out, void *stream);
+
+/* Batched solve_brute: exhaustive vertex evaluation (the check).  vertices (B,)
+ * = nonsingular vertices evaluated.  Returns LAD_E_TOO_LARGE when p >
+ * max_variables or C(n+p, p) > max_candidates (whole batch, like the reference). */
+int lad_brute_solve_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                        int32_t max_variables, int64_t max_candidates, double lambda_floor, double *beta,
+                        double *objective, int64_t *vertices, void *stream);
+
+/* evaluate_objective for (B, p) coefficient vectors. */
+int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                      const double *beta, double lambda_floor, double *objective, void *stream);
+
+/* Device-side problem generation for the BASELINE.json configs:
+ *   config 0/2: X~N(0,1), 2 nonzeros +-U[1,3], Laplace(0,0.5), 10% rows +-10
+ *   config 1:   X~U(-1,1), beta~N(0,1), Laplace(0,0.3), lambda~U(0.1,2)
+ *   config 4:   X~t(3), 3 nonzeros +-U[1,3], Cauchy(0,0.2)
+ * Problem i uses counter-based Philox keyed by (seed, first + i), so any shard
+ * [first, first+B) is reproducible independently.  lam may be NULL except for config 1. */
+int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, int64_t B, int32_t n, int32_t p, double *X,
+                     double *Y, double *lam, double *beta_true, void *stream);
+
+/* Config 3: gather the k-th `keep`-row subset (lexicographic itertools.combinations
+ * order) of one dataset (n0, p) for k in [first, first+B). */
+int lad_subsets_f64(const double *X0, const double *Y0, int32_t n0, int32_t p, int32_t keep, int64_t first, int64_t B,
+                    double *X, double *Y, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

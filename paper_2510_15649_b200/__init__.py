@@ -1,0 +1,24 @@
+"""B200-native batched LAD-LASSO solver (drop-in for arxiv/paper_2510_15649's ladlasso hot path).
+
+The reference's solver entry points -- ``solve_locus`` (ternary-chop and
+quadrature), ``ccd_descend`` and ``solve_brute`` -- run as hand-written sm_100a
+CUDA kernels behind the C ABI in include/ladlasso_b200.h, batched over
+(B, n, p) problems.  See DESIGN.md.
+"""
+
+from .config import Bracket, CcdConfig, LocusConfig
+from .errors import (DegenerateInputError, DeviceError, DimensionMismatchError, InvalidInputError,
+                     ProblemTooLargeError, UnboundedDirectionError)
+from .solver import (BatchedSolveResult, Coefficients, Dataset, ProblemSpec, SolveResult, ccd_descend,
+                     ccd_descend_batched, evaluate_objective, evaluate_objective_batched, solve_brute,
+                     solve_brute_batched, solve_ccd, solve_locus, solve_locus_batched)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchedSolveResult", "Bracket", "CcdConfig", "Coefficients", "Dataset", "DegenerateInputError", "DeviceError",
+    "DimensionMismatchError", "InvalidInputError", "LocusConfig", "ProblemSpec", "ProblemTooLargeError",
+    "SolveResult", "UnboundedDirectionError", "ccd_descend", "ccd_descend_batched", "evaluate_objective",
+    "evaluate_objective_batched", "solve_brute", "solve_brute_batched", "solve_ccd", "solve_locus",
+    "solve_locus_batched",
+]

@@ -1,0 +1,1009 @@
+// lad_locus.cuh -- batched LAD-LASSO locus solver for sm_100a.
+//
+// Mapping: one thread per problem (the paper's "one GPU thread per problem",
+// north_star), persistent grid, per-lane work stealing through one atomic
+// counter.  The reference's nested control flow
+//   solve_locus -> axis scan -> expand/ternary/quadrature -> _CurveEvaluator
+//   -> locus_value -> ccd_descend -> sweep -> coordinate step
+// (locus.py:300-409, :150-297; linesearch.py:172-268; ccd.py:126-206) is
+// restated as a resumable state machine (`Ctl`, `controller`) that emits one
+// *descent request* at a time.  The kernel's main loop executes exactly one
+// coordinate step per iteration for every live lane, so all 32 lanes of a
+// warp run the same hot code no matter where each problem is in its solve;
+// only the per-descent bookkeeping (residual init, fresh objective, the
+// controller) diverges.
+//
+// Shared memory per warp (interleaved by lane, conflict-free LDS.64):
+//   Xs[i][j][lane]  design matrix of the lane's problem
+//   Ys[i][lane]     response
+//   Ls[i][lane]     unsorted breakpoints of the current step
+// Registers: residual r[n], the (key, idx) sort arrays, beta[p].
+// Global scratch: per-lane `seen` list of (t, beta) curve points for the
+// nearest-point warm start (locus.py:188-191).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lad_numerics.cuh"
+#include "lad_sortnet.cuh"
+
+namespace lad {
+
+struct LocusParamsDev {
+    int32_t outer_axis;           // -1 = scan all axes by influence
+    int32_t outer_search;         // 0 ternary, 1 quadrature
+    double outer_tolerance;
+    int32_t outer_probes;
+    int32_t outer_max_iterations;
+    int32_t has_bracket;
+    double bracket_lo, bracket_hi;
+    double inner_sweep_tol;
+    int32_t inner_max_sweeps;
+    double lambda_floor;
+};
+
+enum : int { MODE_LOCUS = 0, MODE_DESCENT = 1 };
+
+struct LocusArgs {
+    const double *X;        // (Bd, n, p) row-major
+    const double *Y;        // (Bd, n)
+    const double *lam;      // (B,) raw lambda per problem
+    const int64_t *data_index;  // (B,) problem -> dataset row, or null (identity)
+    int64_t B;
+    int n, p;
+    LocusParamsDev prm;
+    int mode;
+    const double *start;    // MODE_DESCENT: (B, p)
+    const int32_t *frozen;  // MODE_DESCENT: (B,) -1 = none
+    double desc_tol;        // MODE_DESCENT sweep tolerance
+    int desc_sweeps;        // MODE_DESCENT max sweeps
+    // outputs
+    double *beta;           // (B, p)
+    double *objective;      // (B,)
+    int32_t *iterations;    // (B,)
+    int32_t *objective_evals;
+    uint8_t *converged;
+    uint8_t *status;        // 0 ok, 1 unbounded direction, 2 invalid input
+    int32_t *descents;      // may be null
+    int64_t *steps;         // may be null
+    // scratch
+    double *seen;           // per lane slot: seen_cap * (1 + PMAX) doubles
+    int seen_cap;
+    unsigned long long *counter;
+};
+
+template <int PMAX>
+struct Point {
+    double t;
+    double beta[PMAX];
+    double value;
+    int conv;
+};
+
+enum : int {
+    PC_FETCH = 0,
+    PC_AXIS_START,
+    PC_EX_0, PC_EX_1, PC_EX_2, PC_EX_LOOP, PC_EX_MID, PC_EX_NEWLO, PC_EX_NEWHI, PC_EX_BOTH1, PC_EX_BOTH2,
+    PC_OT_START, PC_OT_LOOP, PC_OT_V1, PC_OT_V2, PC_OQ_LOOP, PC_OQ_PROBE, PC_OUTER_END,
+    PC_AXIS_DONE,
+    PC_REFINE_START, PC_REF_AXIS_START, PC_REF_FAN, PC_REF_FAN_AFTER, PC_REF_FAN_REFINED, PC_REF_FAN_FINISH,
+    PC_REF_ROUND, PC_REF_GRID_NEXT, PC_REF_AXIS_DONE,
+    PC_POLISH, PC_POLISH_AFTER,
+    PC_PR_BEGIN, PC_PR_AFTER_COLD, PC_PR_AFTER_WARM, PC_PR_AFTER_FAST_ONLY, PC_PR_REFINE_CHECK,
+    PC_PR_AFTER_REFINE, PC_PR_FINISH,
+    PC_DESC_AFTER,
+};
+
+enum : int { ACT_DESCENT = 0, ACT_EXIT = 1 };
+
+template <int PMAX>
+struct Ctl {
+    // problem
+    int64_t prob;
+    double lam;
+    uint32_t sparse_mask;
+    int pc, ret_pc;
+    // descent request / result
+    double req_start[PMAX];
+    int req_frozen;
+    double req_tol;
+    int req_sweeps;
+    double res_beta[PMAX];
+    double res_obj;
+    int res_conv, res_steps, res_sweeps;
+    // probe
+    double probe_t, probe_v;
+    int warm_idx;
+    Point<PMAX> pt;
+    // evaluator (_CurveEvaluator)
+    int axis, nseen, ev_calls, ev_failures, has_best;
+    Point<PMAX> ev_best;
+    double fast_tol, inner_tol, margin_scale;
+    int fast_sweeps, inner_sweeps, economy;
+    // solve level
+    int axes[PMAX];
+    int naxes, a_idx;
+    double R_lo, R_hi;
+    Point<PMAX> best;
+    int best_axis;
+    double axis_values[PMAX];
+    int nvals, rounds, calls, failures, outer_ok, confirmations;
+    // expand / outer
+    double lo, hi, g_lo, g_hi, target, m1, m2, v1, h, bt, bv;
+    int ex_it, orounds, qk, oconv;
+    // refine
+    int passes, fan, nref, refine_axes[PMAX], ps, q, improved, fan_i, rr, gk;
+    double width, margin, w, ga, gb, gstep, gdelta;
+    Point<PMAX> seeded;
+    Pcg32 rng;
+    // counters
+    int D;
+    long long S;
+};
+
+// ---------------------------------------------------------------------------
+// helpers used by the controller (cold path)
+// ---------------------------------------------------------------------------
+
+template <int NMAX, int PMAX>
+__device__ __forceinline__ double xs_at(const double *Xs, int i, int j, int lane)
+{
+    return Xs[(i * PMAX + j) * 32 + lane];
+}
+
+// np.abs(x).sum(axis=0)[j]: sequential over rows for d >= 2, pairwise for d == 1
+template <int NMAX, int PMAX>
+__device__ double col_abs_sum(const double *Xs, int n, int p, int j, int lane)
+{
+    if (p == 1) return np_sum(n, [&](int i) { return fabs(xs_at<NMAX, PMAX>(Xs, i, 0, lane)); });
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = dadd(s, fabs(xs_at<NMAX, PMAX>(Xs, i, j, lane)));
+    return s;
+}
+
+template <int NMAX, int PMAX>
+__device__ double objective_of(const double *Xs, const double *Ys, int n, int p, int lane, double lam,
+                               const double *b)
+{
+    double rs = np_sum(n, [&](int i) {
+        double g = gemv_row(p, i, n, [&](int jj) { return xs_at<NMAX, PMAX>(Xs, i, jj, lane); },
+                            [&](int jj) { return b[jj]; });
+        return fabs(dsub(Ys[i * 32 + lane], g));
+    });
+    double bs = np_sum(p, [&](int jj) { return fabs(b[jj]); });
+    return dadd(rs, dmul(lam, bs));
+}
+
+#define ISSUE(START_EXPR, FROZEN, TOL, SWEEPS, NEXT)                    \
+    do {                                                                \
+        for (int jj_ = 0; jj_ < p; ++jj_) C.req_start[jj_] = (START_EXPR); \
+        C.req_frozen = (FROZEN);                                        \
+        C.req_tol = (TOL);                                              \
+        C.req_sweeps = (SWEEPS);                                        \
+        C.pc = (NEXT);                                                  \
+        return ACT_DESCENT;                                             \
+    } while (0)
+
+#define PROBE(T, RET)            \
+    do {                         \
+        C.probe_t = (T);         \
+        C.ret_pc = (RET);        \
+        C.pc = PC_PR_BEGIN;      \
+        goto next_state;         \
+    } while (0)
+
+template <int PMAX>
+__device__ __forceinline__ void set_point_from_result(Ctl<PMAX> &C, Point<PMAX> &P, double t, int p)
+{
+    P.t = t;
+    for (int j = 0; j < p; ++j) P.beta[j] = C.res_beta[j];
+    P.value = C.res_obj;
+    P.conv = C.res_conv;
+}
+
+template <int PMAX>
+__device__ __forceinline__ void seen_append(const LocusArgs &A, double *seen, Ctl<PMAX> &C, const Point<PMAX> &P,
+                                            int p)
+{
+    if (seen == nullptr) return;
+    int k = C.nseen;
+    if (k < A.seen_cap) {
+        seen[k] = P.t;
+        double *sb = seen + A.seen_cap + (size_t)k * PMAX;
+        for (int j = 0; j < p; ++j) sb[j] = P.beta[j];
+    }
+    C.nseen = k + 1;
+}
+
+template <int PMAX>
+__device__ __forceinline__ void evaluator_reset(Ctl<PMAX> &C, int axis, const LocusArgs &A, int p)
+{
+    C.axis = axis;
+    C.nseen = 0;
+    C.ev_calls = 0;
+    C.ev_failures = 0;
+    C.has_best = 0;
+    C.economy = p > 3;
+    double tol = A.prm.inner_sweep_tol;
+    int ms = A.prm.inner_max_sweeps;
+    C.inner_tol = tol;
+    C.inner_sweeps = C.economy ? (ms < 150 ? ms : 150) : ms;
+    C.fast_tol = tol > 1e-7 ? tol : 1e-7;
+    int cap = C.economy ? 40 : 150;
+    C.fast_sweeps = ms < cap ? ms : cap;
+    C.margin_scale = C.economy ? 1e-4 : 1e-3;
+}
+
+// ---------------------------------------------------------------------------
+// controller: advances the lane's state machine until the next descent
+// ---------------------------------------------------------------------------
+template <int NMAX, int PMAX, bool EXACT>
+__device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double *Xs, double *Ys, int lane,
+                                       int slot)
+{
+    const int n = EXACT ? NMAX : A.n;
+    const int p = EXACT ? PMAX : A.p;
+    double *seen = (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PMAX) : nullptr;
+    for (;;) {
+        switch (C.pc) {
+        case PC_FETCH: {
+            unsigned long long pr = atomicAdd(A.counter, 1ULL);
+            if ((int64_t)pr >= A.B) return ACT_EXIT;
+            C.prob = (int64_t)pr;
+            int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
+            const double *xg = A.X + (size_t)src * n * p;
+            const double *yg = A.Y + (size_t)src * n;
+            bool ok = true;
+            uint32_t mask = 0;
+            for (int i = 0; i < n; ++i) {
+                double yv = yg[i];
+                ok = ok && isfinite(yv);
+                Ys[i * 32 + lane] = yv;
+                for (int j = 0; j < p; ++j) {
+                    double xv = xg[i * p + j];
+                    ok = ok && isfinite(xv);
+                    if (xv == 0.0) mask |= 1u << j;
+                    Xs[(i * PMAX + j) * 32 + lane] = xv;
+                }
+            }
+            double lraw = A.lam[pr];
+            ok = ok && isfinite(lraw) && lraw >= 0.0;
+            C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
+            C.sparse_mask = mask;
+            C.D = 0;
+            C.S = 0;
+            if (!ok) {
+                for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
+                A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
+                A.iterations[pr] = 0;
+                A.objective_evals[pr] = 0;
+                A.converged[pr] = 0;
+                A.status[pr] = 2;
+                if (A.descents) A.descents[pr] = 0;
+                if (A.steps) A.steps[pr] = 0;
+                continue;  // fetch next
+            }
+            if (A.mode == MODE_DESCENT) {
+                const double *st = A.start + (size_t)pr * p;
+                int fr = A.frozen ? A.frozen[pr] : -1;
+                ISSUE(st[jj_], fr, A.desc_tol, A.desc_sweeps, PC_DESC_AFTER);
+            }
+            // axes_by_influence (locus.py:90-93) and default_bracket (:96-101)
+            double infl[PMAX];
+            double scale = 0.0;
+            for (int j = 0; j < p; ++j) {
+                double s = col_abs_sum<NMAX, PMAX>(Xs, n, p, j, lane);
+                infl[j] = s;
+                double mean = ddiv(s, (double)n);
+                if (j == 0 || mean > scale) scale = mean;
+            }
+            if (A.prm.outer_axis >= 0) {
+                C.axes[0] = A.prm.outer_axis;
+                C.naxes = 1;
+            } else {
+                for (int j = 0; j < p; ++j) {
+                    int k = j;
+                    while (k > 0 && -infl[C.axes[k - 1]] > -infl[j]) {
+                        C.axes[k] = C.axes[k - 1];
+                        --k;
+                    }
+                    C.axes[k] = j;
+                }
+                C.naxes = p;
+            }
+            if (A.prm.has_bracket) {
+                C.R_lo = A.prm.bracket_lo;
+                C.R_hi = A.prm.bracket_hi;
+            } else {
+                double ymax = 0.0;
+                for (int i = 0; i < n; ++i) {
+                    double a = fabs(Ys[i * 32 + lane]);
+                    if (i == 0 || a > ymax) ymax = a;
+                }
+                double radius = scale > 0.0 ? ddiv(ymax, scale) : __longlong_as_double(0x7ff0000000000000LL);
+                if (!isfinite(radius) || radius <= 0.0) radius = 1.0;
+                C.R_lo = -radius;
+                C.R_hi = radius;
+            }
+            C.a_idx = 0;
+            C.best_axis = C.axes[0];
+            C.nvals = C.rounds = C.calls = C.failures = 0;
+            C.outer_ok = 1;
+            C.confirmations = 0;
+            C.pc = PC_AXIS_START;
+            break;
+        }
+        case PC_DESC_AFTER: {
+            int64_t pr = C.prob;
+            for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = C.res_beta[j];
+            A.objective[pr] = C.res_obj;
+            A.iterations[pr] = C.res_sweeps;
+            A.objective_evals[pr] = C.res_steps;
+            A.converged[pr] = (uint8_t)C.res_conv;
+            A.status[pr] = 0;
+            if (A.descents) A.descents[pr] = C.D;
+            if (A.steps) A.steps[pr] = C.S;
+            C.pc = PC_FETCH;
+            break;
+        }
+        // ------------------------------------------------ axis search
+        case PC_AXIS_START: {
+            evaluator_reset(C, C.axes[C.a_idx], A, p);
+            C.lo = C.R_lo;
+            C.hi = C.R_hi;
+            C.pc = PC_EX_0;
+            break;
+        }
+        // expand_bracket (linesearch.py:247-268)
+        case PC_EX_0: PROBE(C.lo, PC_EX_1);
+        case PC_EX_1: C.g_lo = C.probe_v; PROBE(C.hi, PC_EX_2);
+        case PC_EX_2: C.g_hi = C.probe_v; C.ex_it = 0; C.pc = PC_EX_LOOP; break;
+        case PC_EX_LOOP: {
+            if (C.ex_it >= 60) {  // UnboundedDirectionError
+                int64_t pr = C.prob;
+                for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
+                A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
+                A.iterations[pr] = C.rounds;
+                A.objective_evals[pr] = C.calls;
+                A.converged[pr] = 0;
+                A.status[pr] = 1;
+                if (A.descents) A.descents[pr] = C.D;
+                if (A.steps) A.steps[pr] = C.S;
+                C.pc = PC_FETCH;
+                break;
+            }
+            PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_EX_MID);
+        }
+        case PC_EX_MID: {
+            double g_mid = C.probe_v;
+            if (g_mid < C.g_lo && g_mid < C.g_hi) {
+                C.pc = PC_OT_START;
+                break;
+            }
+            double step = dmul(1.0, dsub(C.hi, C.lo));
+            if (C.g_lo < C.g_hi) {
+                C.lo = dsub(C.lo, step);
+                PROBE(C.lo, PC_EX_NEWLO);
+            } else if (C.g_hi < C.g_lo) {
+                C.hi = dadd(C.hi, step);
+                PROBE(C.hi, PC_EX_NEWHI);
+            } else {
+                C.lo = dsub(C.lo, step);
+                C.hi = dadd(C.hi, step);
+                PROBE(C.lo, PC_EX_BOTH1);
+            }
+        }
+        case PC_EX_NEWLO: C.g_lo = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
+        case PC_EX_NEWHI: C.g_hi = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
+        case PC_EX_BOTH1: C.g_lo = C.probe_v; PROBE(C.hi, PC_EX_BOTH2);
+        case PC_EX_BOTH2: C.g_hi = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
+        // ternary_min / quadrature_min (linesearch.py:172-233)
+        case PC_OT_START: {
+            C.target = dmul(A.prm.outer_tolerance, dsub(C.hi, C.lo));
+            C.orounds = 0;
+            PROBE(dmul(0.5, dadd(C.lo, C.hi)), A.prm.outer_search == 0 ? PC_OT_LOOP : PC_OQ_LOOP);
+        }
+        case PC_OT_LOOP: {
+            if (dsub(C.hi, C.lo) > C.target && C.orounds < A.prm.outer_max_iterations) {
+                double third = ddiv(dsub(C.hi, C.lo), 3.0);
+                C.m1 = dadd(C.lo, third);
+                C.m2 = dsub(C.hi, third);
+                PROBE(C.m1, PC_OT_V1);
+            }
+            PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_OUTER_END);
+        }
+        case PC_OT_V1: C.v1 = C.probe_v; PROBE(C.m2, PC_OT_V2);
+        case PC_OT_V2: {
+            if (C.v1 < C.probe_v) C.hi = C.m2;
+            else C.lo = C.m1;
+            C.orounds++;
+            C.pc = PC_OT_LOOP;
+            break;
+        }
+        case PC_OQ_LOOP: {
+            if (dsub(C.hi, C.lo) > C.target && C.orounds < A.prm.outer_max_iterations) {
+                C.h = ddiv(dsub(C.hi, C.lo), (double)(A.prm.outer_probes + 1));
+                C.qk = 1;
+                PROBE(dadd(C.lo, dmul(C.h, 1.0)), PC_OQ_PROBE);
+            }
+            PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_OUTER_END);
+        }
+        case PC_OQ_PROBE: {
+            double t = dadd(C.lo, dmul(C.h, (double)C.qk));
+            if (C.qk == 1 || C.probe_v < C.bv) {
+                C.bv = C.probe_v;
+                C.bt = t;
+            }
+            C.qk++;
+            if (C.qk <= A.prm.outer_probes) PROBE(dadd(C.lo, dmul(C.h, (double)C.qk)), PC_OQ_PROBE);
+            double nlo = dsub(C.bt, C.h), nhi = dadd(C.bt, C.h);
+            C.lo = nlo > C.lo ? nlo : C.lo;
+            C.hi = nhi < C.hi ? nhi : C.hi;
+            C.orounds++;
+            C.pc = PC_OQ_LOOP;
+            break;
+        }
+        case PC_OUTER_END: {
+            C.oconv = dsub(C.hi, C.lo) <= C.target;
+            C.pc = PC_AXIS_DONE;
+            break;
+        }
+        // axis agreement bookkeeping (locus.py:338-362)
+        case PC_AXIS_DONE: {
+            Point<PMAX> &ab = C.ev_best;
+            C.axis_values[C.nvals++] = ab.value;
+            C.rounds += C.orounds;
+            C.calls += C.ev_calls;
+            C.failures += C.ev_failures;
+            C.outer_ok = C.outer_ok && C.oconv;
+            double agree = dmul(p > 3 ? 1e-6 : 1e-7, C.a_idx == 0 ? 1.0 : fmax(1.0, fabs(C.best.value)));
+            bool brk = false;
+            if (C.a_idx == 0) {
+                C.best = ab;
+                C.best_axis = C.axis;
+                C.confirmations = 1;
+            } else if (ab.value < dsub(C.best.value, agree)) {
+                C.best = ab;
+                C.best_axis = C.axis;
+                C.confirmations = 1;
+            } else if (fabs(dsub(ab.value, C.best.value)) <= agree) {
+                C.confirmations += 1;
+            }
+            if (p > 3 && C.confirmations >= 2) brk = true;
+            C.a_idx++;
+            C.pc = (brk || C.a_idx >= C.naxes) ? PC_REFINE_START : PC_AXIS_START;
+            break;
+        }
+        // dense refinement plan (locus.py:363-395)
+        case PC_REFINE_START: {
+            if (p <= 2) {
+                C.pc = PC_POLISH;
+                break;
+            }
+            C.width = dmul(0.01, dsub(C.R_hi, C.R_lo));
+            double vmax = C.axis_values[0], vmin = C.axis_values[0];
+            for (int k = 1; k < C.nvals; ++k) {
+                if (C.axis_values[k] > vmax) vmax = C.axis_values[k];
+                if (C.axis_values[k] < vmin) vmin = C.axis_values[k];
+            }
+            double spread = dsub(vmax, vmin);
+            bool disagree = spread > dmul(1e-7, fmax(1.0, fabs(C.best.value)));
+            if (p == 3 && disagree) {
+                C.passes = 4;
+                C.fan = 12;
+                C.nref = p;
+                for (int j = 0; j < p; ++j) C.refine_axes[j] = j;
+            } else {
+                C.passes = 1;
+                C.nref = 1;
+                C.refine_axes[0] = C.best_axis;
+                C.fan = p == 3 ? 0 : 4;
+            }
+            C.ps = 0;
+            C.q = 0;
+            C.improved = 0;
+            C.pc = PC_REF_AXIS_START;
+            break;
+        }
+        case PC_REF_AXIS_START: {
+            int axis = C.refine_axes[C.q];
+            evaluator_reset(C, axis, A, p);
+            C.seeded = C.best;
+            C.seeded.t = C.best.beta[axis];
+            C.seeded.conv = 1;
+            seen_append(A, seen, C, C.seeded, p);
+            C.ev_best = C.seeded;
+            C.has_best = 1;
+            C.margin = dmul(C.margin_scale, fmax(1.0, fabs(C.seeded.value)));
+            C.rng.seed(0x5EEDULL + (uint64_t)axis, 54);
+            C.fan_i = 0;
+            C.pc = PC_REF_FAN;
+            break;
+        }
+        case PC_REF_FAN: {
+            if (C.fan_i < C.fan) {
+                double st[PMAX];
+                for (int j = 0; j < p; ++j) {
+                    st[j] = C.seeded.beta[j];
+                    if (j == C.axis) continue;
+                    double u = ddiv((double)C.rng.next(), 4294967296.0);
+                    double du = dadd(-1.0, dmul(dsub(1.0, -1.0), u));
+                    st[j] = dadd(st[j], dmul(du, fmax(1.0, fabs(C.seeded.beta[j]))));
+                }
+                st[C.axis] = C.seeded.t;
+                ISSUE(st[jj_], C.axis, C.fast_tol, C.fast_sweeps, PC_REF_FAN_AFTER);
+            }
+            C.w = C.width;
+            C.rr = 0;
+            C.pc = PC_REF_ROUND;
+            break;
+        }
+        case PC_REF_FAN_AFTER: {
+            set_point_from_result(C, C.pt, C.seeded.t, p);
+            if (C.pt.value <= dadd(C.ev_best.value, C.margin)) {
+                double tt = C.seeded.t;
+                ISSUE(jj_ == C.axis ? tt : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_REF_FAN_REFINED);
+            }
+            C.pc = PC_REF_FAN_FINISH;
+            break;
+        }
+        case PC_REF_FAN_REFINED: {
+            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.seeded.t, p);
+            C.pc = PC_REF_FAN_FINISH;
+            break;
+        }
+        case PC_REF_FAN_FINISH: {
+            C.ev_calls++;
+            seen_append(A, seen, C, C.pt, p);
+            if (C.pt.value < C.ev_best.value) C.ev_best = C.pt;
+            C.fan_i++;
+            C.pc = PC_REF_FAN;
+            break;
+        }
+        case PC_REF_ROUND: {
+            if (C.rr < 4) {
+                double center = C.ev_best.t;
+                C.ga = dsub(center, C.w);
+                C.gb = dadd(center, C.w);
+                C.gdelta = dsub(C.gb, C.ga);
+                C.gstep = ddiv(C.gdelta, 15.0);
+                C.gk = 0;
+                PROBE(C.gstep == 0.0 ? dadd(dmul(ddiv(0.0, 15.0), C.gdelta), C.ga) : dadd(dmul(0.0, C.gstep), C.ga),
+                      PC_REF_GRID_NEXT);
+            }
+            C.pc = PC_REF_AXIS_DONE;
+            break;
+        }
+        case PC_REF_GRID_NEXT: {
+            C.gk++;
+            if (C.gk < 16) {
+                double t;
+                if (C.gk == 15) t = C.gb;
+                else if (C.gstep == 0.0) t = dadd(dmul(ddiv((double)C.gk, 15.0), C.gdelta), C.ga);
+                else t = dadd(dmul((double)C.gk, C.gstep), C.ga);
+                PROBE(t, PC_REF_GRID_NEXT);
+            }
+            C.w = dmul(C.w, 2.0 / 15.0);
+            C.rr++;
+            C.pc = PC_REF_ROUND;
+            break;
+        }
+        case PC_REF_AXIS_DONE: {
+            Point<PMAX> &cand = C.ev_best;
+            C.calls += C.ev_calls;
+            C.failures += C.ev_failures;
+            if (cand.value < dsub(C.best.value, dmul(1e-9, fmax(1.0, fabs(C.best.value))))) C.improved = 1;
+            if (cand.value < C.best.value) C.best = cand;
+            C.q++;
+            if (C.q < C.nref) {
+                C.pc = PC_REF_AXIS_START;
+                break;
+            }
+            C.ps++;
+            if (!C.improved || C.ps >= C.passes) {
+                C.pc = PC_POLISH;
+                break;
+            }
+            C.q = 0;
+            C.improved = 0;
+            C.pc = PC_REF_AXIS_START;
+            break;
+        }
+        // final snap (locus.py:396-409)
+        case PC_POLISH:
+            ISSUE(C.best.beta[jj_], -1, A.prm.inner_sweep_tol, A.prm.inner_max_sweeps, PC_POLISH_AFTER);
+        case PC_POLISH_AFTER: {
+            int64_t pr = C.prob;
+            bool use_pol = C.res_obj <= C.best.value;
+            for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = use_pol ? C.res_beta[j] : C.best.beta[j];
+            A.objective[pr] = use_pol ? C.res_obj : C.best.value;
+            A.iterations[pr] = C.rounds;
+            A.objective_evals[pr] = C.calls;
+            A.converged[pr] = (uint8_t)(C.outer_ok && ((double)C.failures <= dmul(0.1, (double)C.calls)));
+            A.status[pr] = 0;
+            if (A.descents) A.descents[pr] = C.D;
+            if (A.steps) A.steps[pr] = C.S;
+            C.pc = PC_FETCH;
+            break;
+        }
+        // ------------------------------------------------ curve evaluator call
+        case PC_PR_BEGIN: {
+            double t = C.probe_t;
+            int wi = -1;
+            if (seen != nullptr && C.nseen > 0) {
+                int lim = C.nseen < A.seen_cap ? C.nseen : A.seen_cap;
+                double bd = fabs(dsub(seen[0], t));
+                wi = 0;
+                for (int k = 1; k < lim; ++k) {
+                    double dd = fabs(dsub(seen[k], t));
+                    if (dd < bd) {
+                        bd = dd;
+                        wi = k;
+                    }
+                }
+            }
+            C.warm_idx = wi;
+            const double *wb = wi >= 0 ? seen + A.seen_cap + (size_t)wi * PMAX : nullptr;
+            if (C.economy && wi >= 0) ISSUE(jj_ == C.axis ? t : wb[jj_], C.axis, C.fast_tol, C.fast_sweeps,
+                                            PC_PR_AFTER_FAST_ONLY);
+            ISSUE(jj_ == C.axis ? t : 0.0, C.axis, C.fast_tol, C.fast_sweeps, PC_PR_AFTER_COLD);
+        }
+        case PC_PR_AFTER_COLD: {
+            set_point_from_result(C, C.pt, C.probe_t, p);
+            if (C.warm_idx >= 0 && p > 2) {
+                const double *wb = seen + A.seen_cap + (size_t)C.warm_idx * PMAX;
+                double t = C.probe_t;
+                ISSUE(jj_ == C.axis ? t : wb[jj_], C.axis, C.fast_tol, C.fast_sweeps, PC_PR_AFTER_WARM);
+            }
+            C.pc = PC_PR_REFINE_CHECK;
+            break;
+        }
+        case PC_PR_AFTER_WARM: {
+            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
+            C.pc = PC_PR_REFINE_CHECK;
+            break;
+        }
+        case PC_PR_AFTER_FAST_ONLY: {
+            set_point_from_result(C, C.pt, C.probe_t, p);
+            C.pc = PC_PR_REFINE_CHECK;
+            break;
+        }
+        case PC_PR_REFINE_CHECK: {
+            bool refine = !C.has_best ||
+                          C.pt.value <= dadd(C.ev_best.value, dmul(C.margin_scale, fmax(1.0, fabs(C.ev_best.value))));
+            if (refine) {
+                double t = C.probe_t;
+                ISSUE(jj_ == C.axis ? t : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_PR_AFTER_REFINE);
+            }
+            C.pc = PC_PR_FINISH;
+            break;
+        }
+        case PC_PR_AFTER_REFINE: {
+            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
+            C.pc = PC_PR_FINISH;
+            break;
+        }
+        case PC_PR_FINISH: {
+            C.ev_calls++;
+            C.ev_failures += C.pt.conv ? 0 : 1;
+            seen_append(A, seen, C, C.pt, p);
+            if (!C.has_best || C.pt.value < C.ev_best.value) {
+                C.ev_best = C.pt;
+                C.has_best = 1;
+            }
+            C.probe_v = C.pt.value;
+            C.pc = C.ret_pc;
+            break;
+        }
+        default:
+            return ACT_EXIT;
+        }
+    next_state:;
+    }
+}
+
+#undef ISSUE
+#undef PROBE
+
+// ---------------------------------------------------------------------------
+// hot path: one exact coordinate step (ccd.py:160-193)
+// ---------------------------------------------------------------------------
+
+// beta register array accessed with a runtime axis index (select chains, no
+// local memory)
+template <int PMAX>
+__device__ __forceinline__ double bget(const double (&b)[PMAX], int j)
+{
+    double v = b[0];
+#pragma unroll
+    for (int k = 1; k < PMAX; ++k) v = (j == k) ? b[k] : v;
+    return v;
+}
+template <int PMAX>
+__device__ __forceinline__ void bset(double (&b)[PMAX], int j, double v)
+{
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) b[k] = (j == k) ? v : b[k];
+}
+
+// Dense column, compile-time n = NMAX: register sort network.
+// Returns true if the step moved beta_j.
+template <int NMAX, int PMAX>
+__device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, double *Ls,
+                                           int lane, int j, double lam, double &f_cur, double &sum_abs_b)
+{
+    constexpr int NE = NMAX + 1;
+    constexpr int XS = PMAX * 32;  // row stride of Xs in doubles
+    const double *xc = Xs + j * 32 + lane;
+    const double bj = bget(b, j);
+    double key[NE];
+    int idx[NE];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+        double loc = dadd(ddiv(r[i], xc[i * XS]), bj);  // np.divide then += b[j] (ccd.py:165-166)
+        key[i] = loc;
+        idx[i] = i;
+        Ls[i * 32 + lane] = loc;
+    }
+    key[NMAX] = 0.0;
+    idx[NMAX] = NMAX;
+    sort_pairs<NE>(key, idx);
+    auto wsorted = [&](int id) -> double {
+        int ic = id < NMAX ? id : NMAX - 1;
+        double x = xc[ic * XS];
+        return id < NMAX ? fabs(x) : lam;
+    };
+    // cum = sequential cumsum in sorted order; total = cum[-1] (ccd.py:85-86)
+    double c = 0.0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) c = dadd(c, wsorted(idx[k]));
+    const double total = c;
+    const double half = dmul(0.5, total);
+    // k = searchsorted(cum, half, 'left')
+    c = 0.0;
+    bool found = false;
+    int kk = NE;
+    double ck = 0.0, tk = key[NE - 1], tk1 = key[NE - 1];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        c = dadd(c, wsorted(idx[k]));
+        bool hit = !found && (c >= half);
+        if (hit) {
+            kk = k;
+            ck = c;
+            tk = key[k];
+            tk1 = key[k + 1 < NE ? k + 1 : k];
+        }
+        found = found || hit;
+    }
+    double t_new;
+    if (kk + 1 < NE && fabs(dsub(ck, half)) <= dmul(1e-12, total)) t_new = dmul(0.5, dadd(tk, tk1));
+    else t_new = tk;
+    // skip test (ccd.py:172)
+    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
+    // v_new = lam*(sum|b| - |b_j|) + |t - locs| @ weights  (ccd.py:177-180)
+    double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
+    double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, i < NMAX ? Ls[i * 32 + lane] : 0.0)); },
+                                 [&](int i) { return i < NMAX ? fabs(xc[i * XS]) : lam; });
+    double v_new = dadd(constant, dot);
+    if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
+        double delta = dsub(t_new, bj);
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+        sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+        bset(b, j, t_new);
+        f_cur = v_new;
+    }
+}
+
+// General column (zero entries, or runtime n): compacted nonzero rows,
+// stable insertion sort in local memory.  Rare path.
+template <int NMAX, int PMAX>
+__device__ __noinline__ void step_general(double *r, double *b, const double *Xs, int lane, int n, int j,
+                                          double lam, double *f_cur, double *sum_abs_b)
+{
+    constexpr int XS = PMAX * 32;
+    const double *xc = Xs + j * 32 + lane;
+    const double bj = b[j];
+    double loc[NMAX + 1], w[NMAX + 1], zr[NMAX];
+    int ord[NMAX + 1];
+    int k = 0, z = 0;
+    bool dense = true;
+    for (int i = 0; i < n; ++i)
+        if (xc[i * XS] == 0.0) dense = false;
+    for (int i = 0; i < n; ++i) {
+        double x = xc[i * XS];
+        if (x != 0.0) {
+            loc[k] = dense ? dadd(ddiv(r[i], x), bj) : ddiv(dadd(r[i], dmul(x, bj)), x);
+            w[k] = fabs(x);
+            ++k;
+        } else {
+            zr[z++] = fabs(r[i]);
+        }
+    }
+    loc[k] = 0.0;
+    w[k] = lam;
+    const int ne = k + 1;
+    for (int i = 0; i < ne; ++i) {
+        int q = i;
+        while (q > 0 && loc[ord[q - 1]] > loc[i]) {
+            ord[q] = ord[q - 1];
+            --q;
+        }
+        ord[q] = i;
+    }
+    double c = 0.0;
+    for (int i = 0; i < ne; ++i) c = dadd(c, w[ord[i]]);
+    const double total = c;
+    const double half = dmul(0.5, total);
+    c = 0.0;
+    int kk = ne;
+    double ck = 0.0;
+    for (int i = 0; i < ne; ++i) {
+        c = dadd(c, w[ord[i]]);
+        if (c >= half) {
+            kk = i;
+            ck = c;
+            break;
+        }
+    }
+    double t_new;
+    if (kk + 1 < ne && fabs(dsub(ck, half)) <= dmul(1e-12, total))
+        t_new = dmul(0.5, dadd(loc[ord[kk]], loc[ord[kk + 1]]));
+    else
+        t_new = loc[ord[kk < ne - 1 ? kk : ne - 1]];
+    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
+    double constant = dmul(lam, dsub(*sum_abs_b, fabs(bj)));
+    if (z) constant = dadd(constant, np_sum(z, [&](int q) { return zr[q]; }));
+    double dot = blas_ddot(ne, [&](int i) { return fabs(dsub(t_new, loc[i])); }, [&](int i) { return w[i]; });
+    double v_new = dadd(constant, dot);
+    if (v_new < *f_cur) {
+        double delta = dsub(t_new, bj);
+        for (int i = 0; i < n; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+        *sum_abs_b = dadd(*sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+        b[j] = t_new;
+        *f_cur = v_new;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int NMAX, int PMAX>
+__host__ __device__ constexpr size_t smem_doubles_per_warp()
+{
+    return (size_t)NMAX * PMAX * 32 + (size_t)NMAX * 32 + (size_t)(NMAX + 1) * 32;
+}
+
+template <int NMAX, int PMAX, bool EXACT>
+__global__ void __launch_bounds__(32) locus_kernel(LocusArgs A)
+{
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31;
+    double *Xs = smem;
+    double *Ys = Xs + NMAX * PMAX * 32;
+    double *Ls = Ys + NMAX * 32;
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = EXACT ? NMAX : A.n;
+    const int p = EXACT ? PMAX : A.p;
+    constexpr int XS = PMAX * 32;
+
+    Ctl<PMAX> C;
+    C.pc = PC_FETCH;
+    double r[NMAX];
+    double b[PMAX];
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) b[k] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) r[i] = 0.0;
+    double f_cur = 0.0, f_sweep_start = 0.0, sum_abs_b = 0.0, tol = 0.0, lam = 0.0;
+    int j = 0, frozen = -1, sweeps = 0, max_sweeps = 0, steps = 0;
+    uint32_t sparse = 0;
+    bool need_ctl = true;
+
+    for (;;) {
+        if (need_ctl) {
+            int act = controller<NMAX, PMAX, EXACT>(C, A, Xs, Ys, lane, slot);
+            if (act == ACT_EXIT) break;
+            lam = C.lam;
+            sparse = C.sparse_mask;
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) b[k] = k < p ? C.req_start[k] : 0.0;
+            frozen = C.req_frozen;
+            tol = C.req_tol;
+            max_sweeps = C.req_sweeps;
+            // descent init (ccd.py:143-155)
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) {
+                if (i < n) {
+                    double g = gemv_row(p, i, n, [&](int jj) { return Xs[i * XS + jj * 32 + lane]; },
+                                        [&](int jj) { return b[jj]; });
+                    r[i] = dsub(Ys[i * 32 + lane], g);
+                }
+            }
+            double sb = np_sum(p, [&](int jj) { return fabs(b[jj]); });
+            double sr = EXACT ? np_sum_c<NMAX>([&](int i) { return fabs(r[i]); })
+                              : np_sum(n, [&](int i) {
+                                    double v = 0.0;
+#pragma unroll
+                                    for (int q = 0; q < NMAX; ++q) v = (q == i) ? r[q] : v;
+                                    return fabs(v);
+                                });
+            f_cur = dadd(sr, dmul(lam, sb));
+            sweeps = 1;
+            steps = 0;
+            f_sweep_start = f_cur;
+            sum_abs_b = sb;
+            j = (frozen == 0) ? 1 : 0;
+            need_ctl = false;
+            if (j >= p) {  // no free axis: one empty sweep, converged (ccd.py:194-196)
+                C.res_conv = 1;
+                C.res_sweeps = 1;
+                C.res_steps = 0;
+#pragma unroll
+                for (int k = 0; k < PMAX; ++k)
+                    if (k < p) C.res_beta[k] = b[k];
+                C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+                C.D += 1;
+                need_ctl = true;
+                continue;
+            }
+        }
+        // ---- one coordinate step on axis j
+        if (EXACT && !((sparse >> j) & 1u)) {
+            step_dense<NMAX, PMAX>(r, b, Xs, Ls, lane, j, lam, f_cur, sum_abs_b);
+        } else {
+            // rare path (zero entries in column j, or runtime-shape kernel): work on
+            // local copies so the register arrays never have their address taken
+            double rl[NMAX], bl[PMAX];
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) rl[i] = r[i];
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) bl[k] = b[k];
+            double fc = f_cur, sa = sum_abs_b;
+            step_general<NMAX, PMAX>(rl, bl, Xs, lane, n, j, lam, &fc, &sa);
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) r[i] = rl[i];
+#pragma unroll
+            for (int k = 0; k < PMAX; ++k) b[k] = bl[k];
+            f_cur = fc;
+            sum_abs_b = sa;
+        }
+        ++steps;
+        // ---- advance (ccd.py:156-196)
+        int jn = j + 1;
+        if (jn == frozen) ++jn;
+        if (jn < p) {
+            j = jn;
+            continue;
+        }
+        bool done = false;
+        int conv = 0;
+        if (dsub(f_sweep_start, f_cur) < tol) {
+            done = true;
+            conv = 1;
+        } else if (sweeps >= max_sweeps) {
+            done = true;
+        }
+        if (!done) {
+            ++sweeps;
+            f_sweep_start = f_cur;
+            sum_abs_b = np_sum(p, [&](int jj) { return fabs(b[jj]); });
+            j = (frozen == 0) ? 1 : 0;
+            continue;
+        }
+        // ---- descent finished: fresh objective (ccd.py:197)
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k)
+            if (k < p) C.res_beta[k] = b[k];
+        C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+        C.res_conv = conv;
+        C.res_sweeps = sweeps;
+        C.res_steps = steps;
+        C.D += 1;
+        C.S += steps;
+        need_ctl = true;
+    }
+}
+
+}  // namespace lad

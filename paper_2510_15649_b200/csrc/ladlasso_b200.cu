@@ -1,0 +1,367 @@
+// ladlasso_b200.cu -- C ABI over the sm_100a kernels (see include/ladlasso_b200.h).
+//
+// Dispatch picks a compile-time (n, p) instantiation of the locus kernel for
+// the BASELINE.json shapes (register-resident sort network, fully unrolled
+// reduction trees) and a runtime-shape instantiation for everything else.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/ladlasso_b200.h"
+#include "lad_brute.cuh"
+#include "lad_gen.cuh"
+#include "lad_locus.cuh"
+
+#define LAD_VERSION 100
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(expr)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess) return fail(LAD_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+extern "C" int lad_version(void) { return LAD_VERSION; }
+extern "C" const char *lad_last_error(void) { return g_err.c_str(); }
+
+extern "C" void lad_default_params(lad_locus_params *prm)
+{
+    prm->outer_axis = -1;
+    prm->outer_search = LAD_OUTER_TERNARY;
+    prm->outer_tolerance = 1e-9;
+    prm->outer_probes = 8;
+    prm->outer_max_iterations = 200;
+    prm->has_bracket = 0;
+    prm->bracket_lo = -1.0;
+    prm->bracket_hi = 1.0;
+    prm->inner_sweep_tol = 1e-10;
+    prm->inner_max_sweeps = 500;
+    prm->lambda_floor = 1e-9;
+}
+
+static_assert(sizeof(lad_locus_params) == sizeof(lad::LocusParamsDev), "params layout");
+
+namespace {
+
+using KernelFn = void (*)(lad::LocusArgs);
+
+struct Variant {
+    KernelFn fn;
+    int nmax, pmax;
+    size_t smem;
+};
+
+template <int N, int P, bool EXACT>
+Variant make_variant()
+{
+    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double)};
+}
+
+bool pick_variant(int n, int p, Variant &v)
+{
+    // exact instantiations: configs 0/2 (30,5), 1 (10,2), 3 (25,5), 4 (31,8)
+    if (n == 30 && p == 5) v = make_variant<30, 5, true>();
+    else if (n == 10 && p == 2) v = make_variant<10, 2, true>();
+    else if (n == 25 && p == 5) v = make_variant<25, 5, true>();
+    else if (n == 31 && p == 8) v = make_variant<31, 8, true>();
+    else if (n <= 16 && p <= 4) v = make_variant<16, 4, false>();
+    else if (n <= 32 && p <= 8) v = make_variant<32, 8, false>();
+    else return false;
+    return true;
+}
+
+int g_num_sms = 0;
+
+int seen_capacity(const lad_locus_params *prm, int p)
+{
+    if (p <= 2) return 0;
+    long long outer = prm->outer_search == LAD_OUTER_TERNARY
+                          ? 2 + 2LL * prm->outer_max_iterations
+                          : 2 + (long long)prm->outer_probes * prm->outer_max_iterations;
+    long long axis = 2 + 3 * 60 + outer;
+    long long refine = 1 + 12 + 64;
+    long long cap = std::max(axis, refine);
+    return (int)std::min<long long>(cap, 1 << 20);
+}
+
+int run_locus(const double *X, const double *Y, const double *lam, const int64_t *data_index, int64_t B, int n, int p,
+              const lad_locus_params *prm, const lad_locus_out *out, cudaStream_t st, int mode, const double *start,
+              const int32_t *frozen, double desc_tol, int desc_sweeps)
+{
+    if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1 (got %lld, %d, %d)", (long long)B, n, p);
+    if (B == 0) return LAD_OK;
+    if (!out || !out->beta || !out->objective || !out->iterations || !out->objective_evals || !out->converged ||
+        !out->status)
+        return fail(LAD_E_INVALID, "output pointers must be non-null");
+    if (prm->outer_tolerance <= 0) return fail(LAD_E_INVALID, "outer_tolerance must be positive");
+    if (prm->outer_probes < 3) return fail(LAD_E_INVALID, "probes must be at least 3");
+    if (prm->outer_max_iterations < 1) return fail(LAD_E_INVALID, "max_iterations must be at least 1");
+    if (prm->inner_sweep_tol <= 0) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
+    if (prm->inner_max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
+    if (prm->outer_axis >= p) return fail(LAD_E_INVALID, "outer_axis %d out of range for d=%d", prm->outer_axis, p);
+    if (prm->has_bracket && !(prm->bracket_lo < prm->bracket_hi))
+        return fail(LAD_E_INVALID, "bracket needs lo < hi");
+    if (!(prm->lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
+    Variant v;
+    if (!pick_variant(n, p, v)) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+
+    if (g_num_sms == 0) {
+        int dev;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem));
+    if (per_sm < 1) return fail(LAD_E_CUDA, "locus kernel does not fit on an SM (smem %zu)", v.smem);
+    int64_t want = (B + 31) / 32;
+    int64_t grid = std::min<int64_t>(want, (int64_t)g_num_sms * per_sm);
+    int64_t slots = grid * 32;
+
+    lad::LocusArgs A;
+    memset(&A, 0, sizeof A);
+    A.X = X;
+    A.Y = Y;
+    A.lam = lam;
+    A.data_index = data_index;
+    A.B = B;
+    A.n = n;
+    A.p = p;
+    memcpy(&A.prm, prm, sizeof A.prm);
+    A.mode = mode;
+    A.start = start;
+    A.frozen = frozen;
+    A.desc_tol = desc_tol;
+    A.desc_sweeps = desc_sweeps;
+    A.beta = out->beta;
+    A.objective = out->objective;
+    A.iterations = out->iterations;
+    A.objective_evals = out->objective_evals;
+    A.converged = out->converged;
+    A.status = out->status;
+    A.descents = out->descents;
+    A.steps = out->steps;
+    A.seen_cap = mode == lad::MODE_LOCUS ? seen_capacity(prm, p) : 0;
+    size_t seen_bytes = (size_t)slots * A.seen_cap * (1 + v.pmax) * sizeof(double);
+    size_t scratch = seen_bytes + 256;
+    char *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, scratch, st));
+    A.counter = (unsigned long long *)buf;
+    A.seen = A.seen_cap ? (double *)(buf + 256) : nullptr;
+    CK(cudaMemsetAsync(buf, 0, 256, st));
+    v.fn<<<(unsigned)grid, 32, v.smem, st>>>(A);
+    cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(buf, st);
+    if (le != cudaSuccess) return fail(LAD_E_CUDA, "locus kernel launch: %s", cudaGetErrorString(le));
+    return LAD_OK;
+}
+
+}  // namespace
+
+extern "C" int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
+                                   int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                                   const lad_locus_out *out, void *stream)
+{
+    lad_locus_params def;
+    if (!prm) {
+        lad_default_params(&def);
+        prm = &def;
+    }
+    return run_locus(X, Y, lam, data_index, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr, nullptr,
+                     0.0, 0);
+}
+
+extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
+                                   int32_t p, const double *start, const int32_t *frozen, double sweep_tolerance,
+                                   int32_t max_sweeps, double lambda_floor, const lad_locus_out *out, void *stream)
+{
+    if (!(sweep_tolerance > 0)) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
+    if (max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
+    if (!start) return fail(LAD_E_INVALID, "start must be non-null");
+    lad_locus_params prm;
+    lad_default_params(&prm);
+    prm.lambda_floor = lambda_floor;
+    return run_locus(X, Y, lam, nullptr, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
+                     sweep_tolerance, max_sweeps);
+}
+
+extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
+                                        int32_t p, const lad_locus_params *prm, const lad_locus_out *out,
+                                        void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    if (B <= 0) return B == 0 ? LAD_OK : fail(LAD_E_INVALID, "B < 0");
+    size_t bx = (size_t)B * n * p * 8, by = (size_t)B * n * 8, bl = (size_t)B * 8, bb = (size_t)B * p * 8;
+    size_t total = bx + by + bl + bb + B * 8 + B * 4 * 2 + B * 2 + B * 4 + B * 8 + 1024;
+    char *d = nullptr;
+    CK(cudaMallocAsync((void **)&d, total, st));
+    char *q = d;
+    auto take = [&](size_t sz) {
+        char *r = q;
+        q += (sz + 255) & ~(size_t)255;
+        return r;
+    };
+    double *dX = (double *)take(bx), *dY = (double *)take(by), *dL = (double *)take(bl);
+    lad_locus_out dout;
+    dout.beta = (double *)take(bb);
+    dout.objective = (double *)take(B * 8);
+    dout.iterations = (int32_t *)take(B * 4);
+    dout.objective_evals = (int32_t *)take(B * 4);
+    dout.converged = (uint8_t *)take(B);
+    dout.status = (uint8_t *)take(B);
+    dout.descents = out->descents ? (int32_t *)take(B * 4) : nullptr;
+    dout.steps = out->steps ? (int64_t *)take(B * 8) : nullptr;
+    CK(cudaMemcpyAsync(dX, X, bx, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st));
+    int rc = lad_locus_solve_f64(dX, dY, dL, nullptr, B, n, p, prm, &dout, stream);
+    if (rc == LAD_OK) {
+        CK(cudaMemcpyAsync(out->beta, dout.beta, bb, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out->objective, dout.objective, B * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out->iterations, dout.iterations, B * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out->objective_evals, dout.objective_evals, B * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out->converged, dout.converged, B, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(out->status, dout.status, B, cudaMemcpyDeviceToHost, st));
+        if (out->descents) CK(cudaMemcpyAsync(out->descents, dout.descents, B * 4, cudaMemcpyDeviceToHost, st));
+        if (out->steps) CK(cudaMemcpyAsync(out->steps, dout.steps, B * 8, cudaMemcpyDeviceToHost, st));
+    }
+    cudaFreeAsync(d, st);
+    CK(cudaStreamSynchronize(st));
+    return rc;
+}
+
+namespace {
+template <int P>
+int brute_dispatch(const double *X, const double *Y, const double *lam, int64_t B, int n, int64_t C,
+                   double lambda_floor, double *beta, double *objective, int64_t *vertices, cudaStream_t st)
+{
+    lad::BruteArgs A;
+    memset(&A, 0, sizeof A);
+    A.X = X;
+    A.Y = Y;
+    A.lam = lam;
+    A.B = B;
+    A.n = n;
+    A.lambda_floor = lambda_floor;
+    A.C = C;
+    A.beta = beta;
+    A.objective = objective;
+    A.vertices = vertices;
+    if (C <= 4096) {
+        int bs = 128;
+        lad::brute_thread_kernel<P><<<(unsigned)((B + bs - 1) / bs), bs, 0, st>>>(A);
+        cudaError_t le = cudaGetLastError();
+        if (le != cudaSuccess) return fail(LAD_E_CUDA, "brute kernel: %s", cudaGetErrorString(le));
+        return LAD_OK;
+    }
+    A.chunk = 256 * 64;
+    A.nchunks = (C + A.chunk - 1) / A.chunk;
+    if (A.nchunks > 65535) {
+        A.nchunks = 65535;
+        A.chunk = (C + A.nchunks - 1) / A.nchunks;
+    }
+    if (B > 65535) return fail(LAD_E_INVALID, "chunked brute handles at most 65535 problems per call");
+    size_t bytes = (size_t)B * A.nchunks * (sizeof(lad::BruteKey) + 8);
+    char *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, bytes, st));
+    A.partial = (lad::BruteKey *)buf;
+    A.pcount = (unsigned long long *)(buf + (size_t)B * A.nchunks * sizeof(lad::BruteKey));
+    dim3 grid((unsigned)A.nchunks, (unsigned)B);
+    lad::brute_chunk_kernel<P><<<grid, 256, 0, st>>>(A);
+    lad::brute_reduce_kernel<P><<<(unsigned)((B + 127) / 128), 128, 0, st>>>(A);
+    cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(buf, st);
+    if (le != cudaSuccess) return fail(LAD_E_CUDA, "brute kernel: %s", cudaGetErrorString(le));
+    return LAD_OK;
+}
+}  // namespace
+
+extern "C" int lad_brute_solve_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
+                                   int32_t p, int32_t max_variables, int64_t max_candidates, double lambda_floor,
+                                   double *beta, double *objective, int64_t *vertices, void *stream)
+{
+    if (n < 1 || p < 1 || B < 0) return fail(LAD_E_INVALID, "bad shape");
+    if (n > 64) return fail(LAD_E_UNSUPPORTED, "brute supports n <= 64");
+    int64_t C = lad::binom(n + p, p);
+    if (p > max_variables)
+        return fail(LAD_E_TOO_LARGE, "d=%d exceeds the enumeration limit of %d variables", p, max_variables);
+    if (C > max_candidates)
+        return fail(LAD_E_TOO_LARGE, "choose(%d, %d) = %lld candidate subsets exceeds the cap of %lld", n + p, p,
+                    (long long)C, (long long)max_candidates);
+    if (B == 0) return LAD_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (p) {
+    case 1: return brute_dispatch<1>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 2: return brute_dispatch<2>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 3: return brute_dispatch<3>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 4: return brute_dispatch<4>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 5: return brute_dispatch<5>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 6: return brute_dispatch<6>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 7: return brute_dispatch<7>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    case 8: return brute_dispatch<8>(X, Y, lam, B, n, C, lambda_floor, beta, objective, vertices, st);
+    default: return fail(LAD_E_UNSUPPORTED, "brute supports p <= 8");
+    }
+}
+
+extern "C" int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                                 const double *beta, double lambda_floor, double *objective, void *stream)
+{
+    if (n < 1 || p < 1 || p > 8 || B < 0) return fail(LAD_E_INVALID, "bad shape");
+    if (B == 0) return LAD_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned g = (unsigned)((B + 127) / 128);
+    switch (p) {
+    case 1: lad::objective_kernel<1><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 2: lad::objective_kernel<2><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 3: lad::objective_kernel<3><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 4: lad::objective_kernel<4><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 5: lad::objective_kernel<5><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 6: lad::objective_kernel<6><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 7: lad::objective_kernel<7><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 8: lad::objective_kernel<8><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    }
+    CK(cudaGetLastError());
+    return LAD_OK;
+}
+
+extern "C" int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, int64_t B, int32_t n, int32_t p,
+                                double *X, double *Y, double *lam, double *beta_true, void *stream)
+{
+    if (config < 0 || config > 4 || config == 3) return fail(LAD_E_INVALID, "config must be 0, 1, 2 or 4");
+    if (n < 1 || n > 64 || p < 1 || p > 8 || B < 0) return fail(LAD_E_INVALID, "bad shape");
+    if (config == 1 && !lam) return fail(LAD_E_INVALID, "config 1 draws lambda per problem: lam must be non-null");
+    if (B == 0) return LAD_OK;
+    lad::GenArgs G{config, seed, first, B, n, p, X, Y, lam, beta_true};
+    lad::gen_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(G);
+    CK(cudaGetLastError());
+    return LAD_OK;
+}
+
+extern "C" int lad_subsets_f64(const double *X0, const double *Y0, int32_t n0, int32_t p, int32_t keep, int64_t first,
+                               int64_t B, double *X, double *Y, void *stream)
+{
+    if (keep < 1 || keep > n0 || n0 > 64 || p < 1 || B < 0) return fail(LAD_E_INVALID, "bad subset shape");
+    if (first < 0 || first + B > lad::binom(n0, keep)) return fail(LAD_E_INVALID, "subset index out of range");
+    if (B == 0) return LAD_OK;
+    lad::subsets_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(X0, Y0, n0, p, keep, first, B,
+                                                                                       X, Y);
+    CK(cudaGetLastError());
+    return LAD_OK;
+}

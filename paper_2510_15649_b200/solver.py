@@ -1,0 +1,408 @@
+"""Batched drop-in for the reference's solver entry points.
+
+Reference boundary (pure Python, /root/reference/pkg/src/ladlasso):
+  locus.solve_locus(spec, cfg)              locus.py:300-409
+  ccd.ccd_descend(spec, start, cfg)         ccd.py:126-206
+  brute.solve_brute(spec, caps)             brute.py:106-145
+  model.evaluate_objective(spec, beta)      model.py:151-154
+Here each becomes one call over B problems (X (B, n, p), y (B, n), lam (B,)).
+Host (numpy) inputs go through the host-buffer C entry point (the copies are
+part of the call); CUDA torch tensors stay on the device and run on the
+current torch stream.  There is no CPU implementation behind any of these.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .config import DEFAULT_LAMBDA_FLOOR, CcdConfig, LocusConfig, locus_params
+from .errors import (DeviceError, DimensionMismatchError, InvalidInputError, ProblemTooLargeError,
+                     UnboundedDirectionError)
+
+STATUS_OK = 0
+STATUS_UNBOUNDED = 1
+STATUS_INVALID = 2
+
+
+def _is_torch(a) -> bool:
+    try:
+        import torch
+
+        return isinstance(a, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def _check(rc: int):
+    if rc == _lib.LAD_OK:
+        return
+    msg = _lib.last_error()
+    if rc == _lib.LAD_E_INVALID:
+        raise InvalidInputError(msg)
+    if rc == _lib.LAD_E_TOO_LARGE:
+        raise ProblemTooLargeError(msg)
+    if rc == _lib.LAD_E_UNSUPPORTED:
+        raise InvalidInputError(msg)
+    raise DeviceError(msg)
+
+
+@dataclass
+class BatchedSolveResult:
+    """Per-problem SolveResult fields (model.py:113-133) as arrays."""
+
+    beta: object            # (B, p)
+    objective: object       # (B,)
+    iterations: object      # (B,) int32
+    objective_evals: object  # (B,) int32
+    converged: object       # (B,) bool
+    status: object          # (B,) uint8: 0 ok, 1 unbounded, 2 invalid
+    descents: object        # (B,) int32: ccd_descend calls
+    steps: object           # (B,) int64: exact coordinate steps
+    solver_id: str
+    wall_time: float
+
+    def raise_for_status(self):
+        st = np.asarray(self.status.cpu() if _is_torch(self.status) else self.status)
+        if (st == STATUS_UNBOUNDED).any():
+            i = int(np.nonzero(st == STATUS_UNBOUNDED)[0][0])
+            raise UnboundedDirectionError(f"problem {i}: no interior minimum found after 60 bracket extensions")
+        if (st == STATUS_INVALID).any():
+            i = int(np.nonzero(st == STATUS_INVALID)[0][0])
+            raise InvalidInputError(f"problem {i}: non-finite data or invalid lambda")
+
+
+def _validate_host(X, y, lam):
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if X.ndim != 3:
+        raise InvalidInputError(f"X must be 3-D (B, n, p), got shape {X.shape}")
+    B, n, p = X.shape
+    if n < 1 or p < 1:
+        raise InvalidInputError(f"need m >= 1 and d >= 1, got {n} x {p}")
+    if y.shape != (B, n):
+        raise DimensionMismatchError(f"y has shape {y.shape}, expected {(B, n)}")
+    lam = np.ascontiguousarray(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)))
+    return X, y, lam
+
+
+def _validate_device(X, y, lam):
+    import torch
+
+    if X.dtype != torch.float64 or y.dtype != torch.float64:
+        raise InvalidInputError("device inputs must be float64")
+    if X.dim() != 3:
+        raise InvalidInputError(f"X must be 3-D (B, n, p), got shape {tuple(X.shape)}")
+    B, n, p = X.shape
+    if tuple(y.shape) != (B, n):
+        raise DimensionMismatchError(f"y has shape {tuple(y.shape)}, expected {(B, n)}")
+    if not torch.is_tensor(lam):
+        lam = torch.full((B,), float(lam), dtype=torch.float64, device=X.device)
+    lam = lam.to(torch.float64).expand(B).contiguous()
+    return X.contiguous(), y.contiguous(), lam
+
+
+def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_floor: float = DEFAULT_LAMBDA_FLOOR,
+                        data_index=None, strict: bool = False, stream=None) -> BatchedSolveResult:
+    """Batched ``solve_locus`` (locus.py:300).  Inputs numpy (host) or CUDA torch tensors."""
+    L = _lib.load()
+    cfg = cfg if cfg is not None else LocusConfig()
+    solver_id = "locus_ternary" if cfg.outer_search == "ternary" else "locus_quadrature"
+    if _is_torch(X):
+        import torch
+
+        X, y, lam = _validate_device(X, y, lam)
+        Bd, n, p = X.shape
+        B = lam.shape[0]
+        if data_index is not None:
+            data_index = data_index.to(device=X.device, dtype=torch.int64).contiguous()
+            B = data_index.shape[0]
+            lam = lam.expand(B).contiguous() if lam.shape[0] == 1 else lam
+        prm = locus_params(cfg, lambda_floor, p)
+        dev = X.device
+        beta = torch.empty((B, p), dtype=torch.float64, device=dev)
+        obj = torch.empty(B, dtype=torch.float64, device=dev)
+        it = torch.empty(B, dtype=torch.int32, device=dev)
+        ev = torch.empty(B, dtype=torch.int32, device=dev)
+        cv = torch.empty(B, dtype=torch.uint8, device=dev)
+        stt = torch.empty(B, dtype=torch.uint8, device=dev)
+        dsc = torch.empty(B, dtype=torch.int32, device=dev)
+        stp = torch.empty(B, dtype=torch.int64, device=dev)
+        out = _lib.LocusOut(beta.data_ptr(), obj.data_ptr(), it.data_ptr(), ev.data_ptr(), cv.data_ptr(),
+                            stt.data_ptr(), dsc.data_ptr(), stp.data_ptr())
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        t0 = time.perf_counter()
+        _check(L.lad_locus_solve_f64(X.data_ptr(), y.data_ptr(), lam.data_ptr(),
+                                     data_index.data_ptr() if data_index is not None else None, B, n, p,
+                                     C.byref(prm), C.byref(out), s))
+        res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
+    else:
+        if data_index is not None:
+            raise InvalidInputError("data_index is supported for device tensors only")
+        X, y, lam = _validate_host(X, y, lam)
+        B, n, p = X.shape
+        prm = locus_params(cfg, lambda_floor, p)
+        beta = np.empty((B, p))
+        obj = np.empty(B)
+        it = np.empty(B, np.int32)
+        ev = np.empty(B, np.int32)
+        cv = np.empty(B, np.uint8)
+        stt = np.empty(B, np.uint8)
+        dsc = np.empty(B, np.int32)
+        stp = np.empty(B, np.int64)
+        out = _lib.LocusOut(*(a.ctypes.data for a in (beta, obj, it, ev, cv, stt, dsc, stp)))
+        t0 = time.perf_counter()
+        _check(L.lad_locus_solve_host_f64(X.ctypes.data, y.ctypes.data, lam.ctypes.data, B, n, p, C.byref(prm),
+                                          C.byref(out), stream))
+        res = BatchedSolveResult(beta, obj, it, ev, cv.astype(bool), stt, dsc, stp, solver_id,
+                                 time.perf_counter() - t0)
+    if strict:
+        res.raise_for_status()
+    return res
+
+
+def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=None, *,
+                        lambda_floor: float = DEFAULT_LAMBDA_FLOOR) -> BatchedSolveResult:
+    """Batched ``ccd_descend`` (ccd.py:126).  ``frozen``: int, None or (B,) array (-1 = none)."""
+    import torch
+
+    L = _lib.load()
+    cfg = cfg if cfg is not None else CcdConfig()
+    if getattr(cfg, "line_search", "exact_median") != "exact_median":
+        raise InvalidInputError("the CUDA path implements line_search='exact_median' only")
+    host = not _is_torch(X)
+    if host:
+        X, y, lam = _validate_host(X, y, lam)
+        dev = torch.device("cuda")
+        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+    else:
+        Xt, yt, lt = _validate_device(X, y, lam)
+        dev = Xt.device
+    B, n, p = Xt.shape
+    st = torch.as_tensor(np.asarray(start, dtype=np.float64) if not _is_torch(start) else start,
+                         dtype=torch.float64, device=dev).reshape(-1, p).expand(B, p).contiguous()
+    if frozen is None and getattr(cfg, "frozen_axis", None) is not None:
+        frozen = cfg.frozen_axis
+    if frozen is None:
+        fr = torch.full((B,), -1, dtype=torch.int32, device=dev)
+    else:
+        fr = torch.as_tensor(frozen if _is_torch(frozen) else np.asarray(frozen), device=dev).to(torch.int32)
+        fr = fr.reshape(-1).expand(B).contiguous()
+        frc = fr.cpu().numpy()
+        if ((frc < -1) | (frc >= p)).any():
+            raise InvalidInputError(f"frozen_axis out of range for d={p}")
+    beta = torch.empty((B, p), dtype=torch.float64, device=dev)
+    obj = torch.empty(B, dtype=torch.float64, device=dev)
+    it = torch.empty(B, dtype=torch.int32, device=dev)
+    ev = torch.empty(B, dtype=torch.int32, device=dev)
+    cv = torch.empty(B, dtype=torch.uint8, device=dev)
+    stt = torch.empty(B, dtype=torch.uint8, device=dev)
+    out = _lib.LocusOut(beta.data_ptr(), obj.data_ptr(), it.data_ptr(), ev.data_ptr(), cv.data_ptr(),
+                        stt.data_ptr(), None, None)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    t0 = time.perf_counter()
+    _check(L.lad_ccd_descend_f64(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, st.data_ptr(), fr.data_ptr(),
+                                 float(cfg.sweep_tolerance), int(cfg.max_sweeps), float(lambda_floor),
+                                 C.byref(out), s))
+    res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, None, None, "ccd_plain", 0.0)
+    if host:
+        torch.cuda.synchronize(dev)
+        res = BatchedSolveResult(beta.cpu().numpy(), obj.cpu().numpy(), it.cpu().numpy(), ev.cpu().numpy(),
+                                 cv.bool().cpu().numpy(), stt.cpu().numpy(), None, None, "ccd_plain",
+                                 time.perf_counter() - t0)
+    return res
+
+
+def solve_brute_batched(X, y, lam, max_variables: int = 6, max_candidates: int = 2_000_000, *,
+                        lambda_floor: float = DEFAULT_LAMBDA_FLOOR):
+    """Batched ``solve_brute`` (brute.py:106).  Returns (beta, objective, vertices)."""
+    import torch
+
+    L = _lib.load()
+    host = not _is_torch(X)
+    if host:
+        X, y, lam = _validate_host(X, y, lam)
+        dev = torch.device("cuda")
+        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+    else:
+        Xt, yt, lt = _validate_device(X, y, lam)
+        dev = Xt.device
+    B, n, p = Xt.shape
+    beta = torch.empty((B, p), dtype=torch.float64, device=dev)
+    obj = torch.empty(B, dtype=torch.float64, device=dev)
+    nv = torch.empty(B, dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    _check(L.lad_brute_solve_f64(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, int(max_variables),
+                                 int(max_candidates), float(lambda_floor), beta.data_ptr(), obj.data_ptr(),
+                                 nv.data_ptr(), s))
+    if host:
+        return beta.cpu().numpy(), obj.cpu().numpy(), nv.cpu().numpy()
+    return beta, obj, nv
+
+
+def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT_LAMBDA_FLOOR):
+    """Batched ``evaluate_objective`` (model.py:151) on the device."""
+    import torch
+
+    L = _lib.load()
+    host = not _is_torch(X)
+    if host:
+        X, y, lam = _validate_host(X, y, lam)
+        dev = torch.device("cuda")
+        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+        bt = torch.from_numpy(np.ascontiguousarray(beta, dtype=np.float64)).to(dev)
+    else:
+        Xt, yt, lt = _validate_device(X, y, lam)
+        dev = Xt.device
+        bt = beta.to(torch.float64).contiguous()
+    B, n, p = Xt.shape
+    out = torch.empty(B, dtype=torch.float64, device=dev)
+    _check(L.lad_objective_f64(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, bt.data_ptr(),
+                               float(lambda_floor), out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    return out.cpu().numpy() if host else out
+
+
+# ---------------------------------------------------------------------------
+# single-problem mirrors of the reference API (B = 1 calls)
+# ---------------------------------------------------------------------------
+
+def _frozen_array(values, ndim, what):
+    out = np.array(values, dtype=float)
+    if out.ndim != ndim:
+        raise InvalidInputError(f"{what} must be {ndim}-D, got shape {out.shape}")
+    if not np.isfinite(out).all():
+        raise InvalidInputError(f"{what} must contain only finite values")
+    out.setflags(write=False)
+    return out
+
+
+@dataclass(frozen=True, eq=False)
+class Dataset:
+    """model.Dataset (model.py:42-66)."""
+
+    x: np.ndarray
+    y: np.ndarray
+
+    def __post_init__(self):
+        x = _frozen_array(self.x, 2, "x")
+        y = _frozen_array(self.y, 1, "y")
+        m, d = x.shape
+        if m < 1 or d < 1:
+            raise InvalidInputError(f"need m >= 1 and d >= 1, got {m} x {d}")
+        if y.shape[0] != m:
+            raise DimensionMismatchError(f"y has {y.shape[0]} entries for {m} data rows")
+        object.__setattr__(self, "x", x)
+        object.__setattr__(self, "y", y)
+
+    @property
+    def m(self):
+        return self.x.shape[0]
+
+    @property
+    def d(self):
+        return self.x.shape[1]
+
+
+@dataclass(frozen=True, eq=False)
+class Coefficients:
+    beta: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "beta", _frozen_array(self.beta, 1, "beta"))
+
+    def __len__(self):
+        return self.beta.shape[0]
+
+    @classmethod
+    def zeros(cls, d):
+        return cls(np.zeros(d))
+
+
+@dataclass(frozen=True, eq=False)
+class ProblemSpec:
+    """model.ProblemSpec (model.py:86-110)."""
+
+    data: Dataset
+    lam: float
+    lambda_floor: float = DEFAULT_LAMBDA_FLOOR
+
+    def __post_init__(self):
+        if not math.isfinite(self.lam) or self.lam < 0:
+            raise InvalidInputError("lam must be finite and >= 0")
+        if not math.isfinite(self.lambda_floor) or self.lambda_floor <= 0:
+            raise InvalidInputError("lambda_floor must be finite and > 0")
+
+    @property
+    def lambda_eff(self):
+        return max(self.lam, self.lambda_floor)
+
+    @property
+    def m(self):
+        return self.data.m
+
+    @property
+    def d(self):
+        return self.data.d
+
+
+@dataclass(frozen=True, eq=False)
+class SolveResult:
+    beta: Coefficients
+    objective: float
+    solver_id: str
+    iterations: int
+    objective_evals: int
+    wall_time: float
+    converged: bool
+
+
+def _spec_arrays(spec):
+    data = spec.data
+    return (np.asarray(data.x, dtype=float)[None], np.asarray(data.y, dtype=float)[None],
+            np.array([float(spec.lam)]), float(getattr(spec, "lambda_floor", DEFAULT_LAMBDA_FLOOR)))
+
+
+def solve_locus(spec, cfg=None) -> SolveResult:
+    """Drop-in for ``ladlasso.locus.solve_locus`` on one problem (runs on the GPU)."""
+    X, y, lam, floor = _spec_arrays(spec)
+    r = solve_locus_batched(X, y, lam, cfg, lambda_floor=floor, strict=True)
+    return SolveResult(Coefficients(r.beta[0]), float(r.objective[0]), r.solver_id, int(r.iterations[0]),
+                       int(r.objective_evals[0]), r.wall_time, bool(r.converged[0]))
+
+
+def ccd_descend(spec, start, cfg=None) -> SolveResult:
+    """Drop-in for ``ladlasso.ccd.ccd_descend`` on one problem (runs on the GPU)."""
+    X, y, lam, floor = _spec_arrays(spec)
+    b = start.beta if hasattr(start, "beta") else np.asarray(start, dtype=float)
+    if b.shape != (X.shape[2],):
+        raise DimensionMismatchError(f"beta has shape {b.shape}, problem has {X.shape[2]} variables")
+    cfg = cfg if cfg is not None else CcdConfig()
+    r = ccd_descend_batched(X, y, lam, b[None], cfg, frozen=cfg.frozen_axis, lambda_floor=floor)
+    return SolveResult(Coefficients(r.beta[0]), float(r.objective[0]), "ccd_plain", int(r.iterations[0]),
+                       int(r.objective_evals[0]), r.wall_time, bool(r.converged[0]))
+
+
+def solve_ccd(spec, cfg=None, start=None) -> SolveResult:
+    return ccd_descend(spec, start if start is not None else np.zeros(spec.d), cfg)
+
+
+def solve_brute(spec, max_variables: int = 6, max_candidates: int = 2_000_000) -> SolveResult:
+    """Drop-in for ``ladlasso.brute.solve_brute`` on one problem (runs on the GPU)."""
+    X, y, lam, floor = _spec_arrays(spec)
+    t0 = time.perf_counter()
+    beta, obj, nv = solve_brute_batched(X, y, lam, max_variables, max_candidates, lambda_floor=floor)
+    return SolveResult(Coefficients(beta[0]), float(obj[0]), "brute", int(nv[0]), int(nv[0]),
+                       time.perf_counter() - t0, True)
+
+
+def evaluate_objective(spec, beta) -> float:
+    X, y, lam, floor = _spec_arrays(spec)
+    b = beta.beta if hasattr(beta, "beta") else np.asarray(beta, dtype=float)
+    if b.shape != (X.shape[2],):
+        raise DimensionMismatchError(f"beta has shape {b.shape}, problem has {X.shape[2]} variables")
+    return float(evaluate_objective_batched(X, y, lam, b[None], lambda_floor=floor)[0])
