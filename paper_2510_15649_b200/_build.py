@@ -16,7 +16,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libladlasso_b200.so")
 SOURCES = ["ladlasso_b200.cu"]
-HEADERS = ["lad_numerics.cuh", "lad_sortnet.cuh", "lad_locus.cuh", "lad_brute.cuh", "lad_gen.cuh"]
+HEADERS = ["lad_numerics.cuh", "lad_sortnet.cuh", "lad_locus.cuh", "lad_locus_warp.cuh", "lad_brute.cuh",
+           "lad_gen.cuh"]
 
 NVCC_FLAGS = [
     "-std=c++17",

@@ -15,6 +15,7 @@ SYMBOLS = (
     "lad_version",
     "lad_last_error",
     "lad_default_params",
+    "lad_set_kernel_policy",
     "lad_locus_solve_f64",
     "lad_locus_solve_host_f64",
     "lad_ccd_descend_f64",
@@ -29,6 +30,17 @@ LAD_E_INVALID = -1
 LAD_E_TOO_LARGE = -2
 LAD_E_CUDA = -3
 LAD_E_UNSUPPORTED = -4
+
+KERNEL_AUTO = 0
+KERNEL_THREAD = 1
+KERNEL_WARP = 2
+
+
+def set_kernel_policy(policy: int) -> None:
+    """Choose the locus kernel mapping (auto / thread-per-problem / warp-per-problem)."""
+    rc = load().lad_set_kernel_policy(policy)
+    if rc != LAD_OK:
+        raise ValueError(last_error())
 
 
 class LocusParams(C.Structure):
@@ -85,6 +97,7 @@ def load(build_if_missing: bool = False):
     L.lad_last_error.restype = C.c_char_p
     L.lad_default_params.argtypes = [C.POINTER(LocusParams)]
     L.lad_default_params.restype = None
+    L.lad_set_kernel_policy.argtypes = [i32]
     L.lad_locus_solve_f64.argtypes = [vp, vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
     L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
     L.lad_ccd_descend_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, dbl, i32, dbl, C.POINTER(LocusOut), vp]

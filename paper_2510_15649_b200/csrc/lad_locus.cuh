@@ -203,11 +203,11 @@ __device__ __forceinline__ void set_point_from_result(Ctl<PMAX> &C, Point<PMAX> 
 
 template <int PMAX>
 __device__ __forceinline__ void seen_append(const LocusArgs &A, double *seen, Ctl<PMAX> &C, const Point<PMAX> &P,
-                                            int p)
+                                            int p, bool leader)
 {
     if (seen == nullptr) return;
     int k = C.nseen;
-    if (k < A.seen_cap) {
+    if (leader && k < A.seen_cap) {
         seen[k] = P.t;
         double *sb = seen + A.seen_cap + (size_t)k * PMAX;
         for (int j = 0; j < p; ++j) sb[j] = P.beta[j];
@@ -234,55 +234,125 @@ __device__ __forceinline__ void evaluator_reset(Ctl<PMAX> &C, int axis, const Lo
     C.margin_scale = C.economy ? 1e-4 : 1e-3;
 }
 
+template <int PMAX>
+__device__ __forceinline__ void write_invalid(const LocusArgs &A, int64_t pr, int p)
+{
+    for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
+    A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
+    A.iterations[pr] = 0;
+    A.objective_evals[pr] = 0;
+    A.converged[pr] = 0;
+    A.status[pr] = 2;
+    if (A.descents) A.descents[pr] = 0;
+    if (A.steps) A.steps[pr] = 0;
+}
+
+// first minimal |seen_t[k] - t| (locus.py:188-191), 8 loads in flight
+__device__ __forceinline__ int nearest_serial(const double *seen, int lim, double t)
+{
+    int wi = -1;
+    double bd = __longlong_as_double(0x7ff0000000000000LL);
+    int k = 0;
+    for (; k + 8 <= lim; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = seen[k + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double dd = fabs(dsub(v[q], t));
+            if (dd < bd) {
+                bd = dd;
+                wi = k + q;
+            }
+        }
+    }
+    for (; k < lim; ++k) {
+        double dd = fabs(dsub(seen[k], t));
+        if (dd < bd) {
+            bd = dd;
+            wi = k;
+        }
+    }
+    return wi;
+}
+
+// Access policy of the thread-per-problem kernel: the lane owns its problem;
+// data lives in the lane's column of the interleaved shared arrays.
+template <int NMAX, int PMAX>
+struct ThreadAccess {
+    int n, p, lane;
+    double *Xs, *Ys;
+    __device__ __forceinline__ bool leader() const { return true; }
+    __device__ __forceinline__ void sync() const {}
+    __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
+    {
+        unsigned long long pr = atomicAdd(A.counter, 1ULL);
+        if ((int64_t)pr >= A.B) return -1;
+        C.prob = (int64_t)pr;
+        int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
+        const double *xg = A.X + (size_t)src * n * p;
+        const double *yg = A.Y + (size_t)src * n;
+        bool ok = true;
+        uint32_t mask = 0;
+        for (int i = 0; i < n; ++i) {
+            double yv = yg[i];
+            ok = ok && isfinite(yv);
+            Ys[i * 32 + lane] = yv;
+            for (int j = 0; j < p; ++j) {
+                double xv = xg[i * p + j];
+                ok = ok && isfinite(xv);
+                if (xv == 0.0) mask |= 1u << j;
+                Xs[(i * PMAX + j) * 32 + lane] = xv;
+            }
+        }
+        double lraw = A.lam[pr];
+        ok = ok && isfinite(lraw) && lraw >= 0.0;
+        C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
+        C.sparse_mask = mask;
+        if (!ok) {
+            write_invalid<PMAX>(A, (int64_t)pr, p);
+            return 0;
+        }
+        return 1;
+    }
+    __device__ double col_abs_sum(int j) const { return lad::col_abs_sum<NMAX, PMAX>(Xs, n, p, j, lane); }
+    __device__ double y_absmax() const
+    {
+        double ymax = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double a = fabs(Ys[i * 32 + lane]);
+            if (i == 0 || a > ymax) ymax = a;
+        }
+        return ymax;
+    }
+    __device__ int nearest(const double *seen, int lim, double t) const { return nearest_serial(seen, lim, t); }
+};
+
 // ---------------------------------------------------------------------------
 // controller: advances the lane's state machine until the next descent
 // ---------------------------------------------------------------------------
-template <int NMAX, int PMAX, bool EXACT>
-__device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double *Xs, double *Ys, int lane,
-                                       int slot)
+// AC (access policy) supplies everything that depends on how a problem is
+// mapped onto threads: fetching the next problem, column sums, the y range,
+// the nearest-seen-point scan, and which thread writes shared results.  The
+// controller itself is the same for the thread-per-problem and the
+// warp-per-problem kernels (in the latter all 32 lanes run it in lock-step
+// on a shared Ctl, with identical values).
+template <int PMAX, class AC>
+__device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const AC &acc, int slot)
 {
-    const int n = EXACT ? NMAX : A.n;
-    const int p = EXACT ? PMAX : A.p;
+    const int n = acc.n;
+    const int p = acc.p;
     double *seen = (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PMAX) : nullptr;
     for (;;) {
+        acc.sync();
         switch (C.pc) {
         case PC_FETCH: {
-            unsigned long long pr = atomicAdd(A.counter, 1ULL);
-            if ((int64_t)pr >= A.B) return ACT_EXIT;
-            C.prob = (int64_t)pr;
-            int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
-            const double *xg = A.X + (size_t)src * n * p;
-            const double *yg = A.Y + (size_t)src * n;
-            bool ok = true;
-            uint32_t mask = 0;
-            for (int i = 0; i < n; ++i) {
-                double yv = yg[i];
-                ok = ok && isfinite(yv);
-                Ys[i * 32 + lane] = yv;
-                for (int j = 0; j < p; ++j) {
-                    double xv = xg[i * p + j];
-                    ok = ok && isfinite(xv);
-                    if (xv == 0.0) mask |= 1u << j;
-                    Xs[(i * PMAX + j) * 32 + lane] = xv;
-                }
-            }
-            double lraw = A.lam[pr];
-            ok = ok && isfinite(lraw) && lraw >= 0.0;
-            C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
-            C.sparse_mask = mask;
+            int got = acc.fetch(C, A);
+            if (got < 0) return ACT_EXIT;
             C.D = 0;
             C.S = 0;
-            if (!ok) {
-                for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
-                A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
-                A.iterations[pr] = 0;
-                A.objective_evals[pr] = 0;
-                A.converged[pr] = 0;
-                A.status[pr] = 2;
-                if (A.descents) A.descents[pr] = 0;
-                if (A.steps) A.steps[pr] = 0;
-                continue;  // fetch next
-            }
+            if (got == 0) continue;  // invalid problem: status written, fetch the next one
+            const int64_t pr = C.prob;
             if (A.mode == MODE_DESCENT) {
                 const double *st = A.start + (size_t)pr * p;
                 int fr = A.frozen ? A.frozen[pr] : -1;
@@ -292,7 +362,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
             double infl[PMAX];
             double scale = 0.0;
             for (int j = 0; j < p; ++j) {
-                double s = col_abs_sum<NMAX, PMAX>(Xs, n, p, j, lane);
+                double s = acc.col_abs_sum(j);
                 infl[j] = s;
                 double mean = ddiv(s, (double)n);
                 if (j == 0 || mean > scale) scale = mean;
@@ -315,11 +385,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
                 C.R_lo = A.prm.bracket_lo;
                 C.R_hi = A.prm.bracket_hi;
             } else {
-                double ymax = 0.0;
-                for (int i = 0; i < n; ++i) {
-                    double a = fabs(Ys[i * 32 + lane]);
-                    if (i == 0 || a > ymax) ymax = a;
-                }
+                double ymax = acc.y_absmax();
                 double radius = scale > 0.0 ? ddiv(ymax, scale) : __longlong_as_double(0x7ff0000000000000LL);
                 if (!isfinite(radius) || radius <= 0.0) radius = 1.0;
                 C.R_lo = -radius;
@@ -335,6 +401,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         }
         case PC_DESC_AFTER: {
             int64_t pr = C.prob;
+            if (acc.leader()) {
             for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = C.res_beta[j];
             A.objective[pr] = C.res_obj;
             A.iterations[pr] = C.res_sweeps;
@@ -343,6 +410,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
             A.status[pr] = 0;
             if (A.descents) A.descents[pr] = C.D;
             if (A.steps) A.steps[pr] = C.S;
+            }
             C.pc = PC_FETCH;
             break;
         }
@@ -361,6 +429,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         case PC_EX_LOOP: {
             if (C.ex_it >= 60) {  // UnboundedDirectionError
                 int64_t pr = C.prob;
+                if (acc.leader()) {
                 for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
                 A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
                 A.iterations[pr] = C.rounds;
@@ -369,6 +438,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
                 A.status[pr] = 1;
                 if (A.descents) A.descents[pr] = C.D;
                 if (A.steps) A.steps[pr] = C.S;
+                }
                 C.pc = PC_FETCH;
                 break;
             }
@@ -511,7 +581,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
             C.seeded = C.best;
             C.seeded.t = C.best.beta[axis];
             C.seeded.conv = 1;
-            seen_append(A, seen, C, C.seeded, p);
+            seen_append(A, seen, C, C.seeded, p, acc.leader());
             C.ev_best = C.seeded;
             C.has_best = 1;
             C.margin = dmul(C.margin_scale, fmax(1.0, fabs(C.seeded.value)));
@@ -554,7 +624,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         }
         case PC_REF_FAN_FINISH: {
             C.ev_calls++;
-            seen_append(A, seen, C, C.pt, p);
+            seen_append(A, seen, C, C.pt, p, acc.leader());
             if (C.pt.value < C.ev_best.value) C.ev_best = C.pt;
             C.fan_i++;
             C.pc = PC_REF_FAN;
@@ -615,6 +685,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         case PC_POLISH_AFTER: {
             int64_t pr = C.prob;
             bool use_pol = C.res_obj <= C.best.value;
+            if (acc.leader()) {
             for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = use_pol ? C.res_beta[j] : C.best.beta[j];
             A.objective[pr] = use_pol ? C.res_obj : C.best.value;
             A.iterations[pr] = C.rounds;
@@ -623,6 +694,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
             A.status[pr] = 0;
             if (A.descents) A.descents[pr] = C.D;
             if (A.steps) A.steps[pr] = C.S;
+            }
             C.pc = PC_FETCH;
             break;
         }
@@ -630,18 +702,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         case PC_PR_BEGIN: {
             double t = C.probe_t;
             int wi = -1;
-            if (seen != nullptr && C.nseen > 0) {
-                int lim = C.nseen < A.seen_cap ? C.nseen : A.seen_cap;
-                double bd = fabs(dsub(seen[0], t));
-                wi = 0;
-                for (int k = 1; k < lim; ++k) {
-                    double dd = fabs(dsub(seen[k], t));
-                    if (dd < bd) {
-                        bd = dd;
-                        wi = k;
-                    }
-                }
-            }
+            if (seen != nullptr && C.nseen > 0) wi = acc.nearest(seen, C.nseen < A.seen_cap ? C.nseen : A.seen_cap, t);
             C.warm_idx = wi;
             const double *wb = wi >= 0 ? seen + A.seen_cap + (size_t)wi * PMAX : nullptr;
             if (C.economy && wi >= 0) ISSUE(jj_ == C.axis ? t : wb[jj_], C.axis, C.fast_tol, C.fast_sweeps,
@@ -686,7 +747,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, double 
         case PC_PR_FINISH: {
             C.ev_calls++;
             C.ev_failures += C.pt.conv ? 0 : 1;
-            seen_append(A, seen, C, C.pt, p);
+            seen_append(A, seen, C, C.pt, p, acc.leader());
             if (!C.has_best || C.pt.value < C.ev_best.value) {
                 C.ev_best = C.pt;
                 C.has_best = 1;
@@ -900,55 +961,67 @@ __global__ void __launch_bounds__(32) locus_kernel(LocusArgs A)
     int j = 0, frozen = -1, sweeps = 0, max_sweeps = 0, steps = 0;
     uint32_t sparse = 0;
     bool need_ctl = true;
+    bool alive = true;
 
+    // Every iteration: (1) lanes at a descent boundary run the controller and
+    // the descent init, (2) all live lanes execute one coordinate step together.
+    // The __syncwarp()s force the lanes back into lock-step after the divergent
+    // bookkeeping, so the hot step always runs with every live lane active.
     for (;;) {
-        if (need_ctl) {
-            int act = controller<NMAX, PMAX, EXACT>(C, A, Xs, Ys, lane, slot);
-            if (act == ACT_EXIT) break;
-            lam = C.lam;
-            sparse = C.sparse_mask;
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, alive)) break;
+        if (alive && need_ctl) {
+            ThreadAccess<NMAX, PMAX> acc{n, p, lane, Xs, Ys};
+            int act = controller<PMAX>(C, A, acc, slot);
+            if (act == ACT_EXIT) {
+                alive = false;
+            } else {
+                lam = C.lam;
+                sparse = C.sparse_mask;
 #pragma unroll
-            for (int k = 0; k < PMAX; ++k) b[k] = k < p ? C.req_start[k] : 0.0;
-            frozen = C.req_frozen;
-            tol = C.req_tol;
-            max_sweeps = C.req_sweeps;
-            // descent init (ccd.py:143-155)
+                for (int k = 0; k < PMAX; ++k) b[k] = k < p ? C.req_start[k] : 0.0;
+                frozen = C.req_frozen;
+                tol = C.req_tol;
+                max_sweeps = C.req_sweeps;
+                // descent init (ccd.py:143-155)
 #pragma unroll
-            for (int i = 0; i < NMAX; ++i) {
-                if (i < n) {
-                    double g = gemv_row(p, i, n, [&](int jj) { return Xs[i * XS + jj * 32 + lane]; },
-                                        [&](int jj) { return b[jj]; });
-                    r[i] = dsub(Ys[i * 32 + lane], g);
+                for (int i = 0; i < NMAX; ++i) {
+                    if (i < n) {
+                        double g = gemv_row(p, i, n, [&](int jj) { return Xs[i * XS + jj * 32 + lane]; },
+                                            [&](int jj) { return b[jj < PMAX ? jj : PMAX - 1]; });
+                        r[i] = dsub(Ys[i * 32 + lane], g);
+                    }
+                }
+                double sb = np_sum(p, [&](int jj) { return fabs(b[jj < PMAX ? jj : PMAX - 1]); });
+                double sr = EXACT ? np_sum_c<NMAX>([&](int i) { return fabs(r[i]); })
+                                  : np_sum(n, [&](int i) {
+                                        double v = 0.0;
+#pragma unroll
+                                        for (int q = 0; q < NMAX; ++q) v = (q == i) ? r[q] : v;
+                                        return fabs(v);
+                                    });
+                f_cur = dadd(sr, dmul(lam, sb));
+                sweeps = 1;
+                steps = 0;
+                f_sweep_start = f_cur;
+                sum_abs_b = sb;
+                j = (frozen == 0) ? 1 : 0;
+                need_ctl = false;
+                if (j >= p) {  // no free axis: one empty sweep, converged (ccd.py:194-196)
+                    C.res_conv = 1;
+                    C.res_sweeps = 1;
+                    C.res_steps = 0;
+#pragma unroll
+                    for (int k = 0; k < PMAX; ++k)
+                        if (k < p) C.res_beta[k] = b[k];
+                    C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+                    C.D += 1;
+                    need_ctl = true;
                 }
             }
-            double sb = np_sum(p, [&](int jj) { return fabs(b[jj]); });
-            double sr = EXACT ? np_sum_c<NMAX>([&](int i) { return fabs(r[i]); })
-                              : np_sum(n, [&](int i) {
-                                    double v = 0.0;
-#pragma unroll
-                                    for (int q = 0; q < NMAX; ++q) v = (q == i) ? r[q] : v;
-                                    return fabs(v);
-                                });
-            f_cur = dadd(sr, dmul(lam, sb));
-            sweeps = 1;
-            steps = 0;
-            f_sweep_start = f_cur;
-            sum_abs_b = sb;
-            j = (frozen == 0) ? 1 : 0;
-            need_ctl = false;
-            if (j >= p) {  // no free axis: one empty sweep, converged (ccd.py:194-196)
-                C.res_conv = 1;
-                C.res_sweeps = 1;
-                C.res_steps = 0;
-#pragma unroll
-                for (int k = 0; k < PMAX; ++k)
-                    if (k < p) C.res_beta[k] = b[k];
-                C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
-                C.D += 1;
-                need_ctl = true;
-                continue;
-            }
         }
+        __syncwarp();
+        if (!alive || need_ctl) continue;
         // ---- one coordinate step on axis j
         if (EXACT && !((sparse >> j) & 1u)) {
             step_dense<NMAX, PMAX>(r, b, Xs, Ls, lane, j, lam, f_cur, sum_abs_b);
@@ -975,34 +1048,34 @@ __global__ void __launch_bounds__(32) locus_kernel(LocusArgs A)
         if (jn == frozen) ++jn;
         if (jn < p) {
             j = jn;
-            continue;
-        }
-        bool done = false;
-        int conv = 0;
-        if (dsub(f_sweep_start, f_cur) < tol) {
-            done = true;
-            conv = 1;
-        } else if (sweeps >= max_sweeps) {
-            done = true;
-        }
-        if (!done) {
-            ++sweeps;
-            f_sweep_start = f_cur;
-            sum_abs_b = np_sum(p, [&](int jj) { return fabs(b[jj]); });
-            j = (frozen == 0) ? 1 : 0;
-            continue;
-        }
-        // ---- descent finished: fresh objective (ccd.py:197)
+        } else {
+            bool done = false;
+            int conv = 0;
+            if (dsub(f_sweep_start, f_cur) < tol) {
+                done = true;
+                conv = 1;
+            } else if (sweeps >= max_sweeps) {
+                done = true;
+            }
+            if (!done) {
+                ++sweeps;
+                f_sweep_start = f_cur;
+                sum_abs_b = np_sum(p, [&](int jj) { return fabs(b[jj < PMAX ? jj : PMAX - 1]); });
+                j = (frozen == 0) ? 1 : 0;
+            } else {
+                // ---- descent finished: fresh objective (ccd.py:197)
 #pragma unroll
-        for (int k = 0; k < PMAX; ++k)
-            if (k < p) C.res_beta[k] = b[k];
-        C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
-        C.res_conv = conv;
-        C.res_sweeps = sweeps;
-        C.res_steps = steps;
-        C.D += 1;
-        C.S += steps;
-        need_ctl = true;
+                for (int k = 0; k < PMAX; ++k)
+                    if (k < p) C.res_beta[k] = b[k];
+                C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+                C.res_conv = conv;
+                C.res_sweeps = sweeps;
+                C.res_steps = steps;
+                C.D += 1;
+                C.S += steps;
+                need_ctl = true;
+            }
+        }
     }
 }
 

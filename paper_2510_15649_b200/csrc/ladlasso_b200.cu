@@ -16,8 +16,9 @@
 #include "lad_brute.cuh"
 #include "lad_gen.cuh"
 #include "lad_locus.cuh"
+#include "lad_locus_warp.cuh"
 
-#define LAD_VERSION 100
+#define LAD_VERSION 101
 
 static thread_local std::string g_err;
 
@@ -65,24 +66,40 @@ using KernelFn = void (*)(lad::LocusArgs);
 struct Variant {
     KernelFn fn;
     int nmax, pmax;
-    size_t smem;
+    size_t smem;      // dynamic shared memory per block
+    int block;        // threads per block
+    int slots_per_block;  // independent solvers (seen-list slots) per block
 };
 
 template <int N, int P, bool EXACT>
-Variant make_variant()
+Variant make_thread_variant()
 {
-    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double)};
+    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double), 32, 32};
 }
+
+template <int P>
+Variant make_warp_variant()
+{
+    return Variant{lad::locus_warp_kernel<P>, 31, P, 0, 32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
+}
+
+int g_kernel_policy = LAD_KERNEL_AUTO;
 
 bool pick_variant(int n, int p, Variant &v)
 {
-    // exact instantiations: configs 0/2 (30,5), 1 (10,2), 3 (25,5), 4 (31,8)
-    if (n == 30 && p == 5) v = make_variant<30, 5, true>();
-    else if (n == 10 && p == 2) v = make_variant<10, 2, true>();
-    else if (n == 25 && p == 5) v = make_variant<25, 5, true>();
-    else if (n == 31 && p == 8) v = make_variant<31, 8, true>();
-    else if (n <= 16 && p <= 4) v = make_variant<16, 4, false>();
-    else if (n <= 32 && p <= 8) v = make_variant<32, 8, false>();
+    const bool warp_ok = n <= 31 && p <= 8;
+    const bool thread_exact = n == 10 && p == 2;  // config 1: thread-per-problem (north_star's tiny-n variant)
+    int policy = g_kernel_policy;
+    if (policy == LAD_KERNEL_AUTO) policy = (thread_exact || !warp_ok) ? LAD_KERNEL_THREAD : LAD_KERNEL_WARP;
+    if (policy == LAD_KERNEL_WARP && warp_ok) {
+        if (p <= 3) v = make_warp_variant<3>();
+        else if (p <= 5) v = make_warp_variant<5>();
+        else v = make_warp_variant<8>();
+        return true;
+    }
+    if (thread_exact) v = make_thread_variant<10, 2, true>();
+    else if (n <= 16 && p <= 4) v = make_thread_variant<16, 4, false>();
+    else if (n <= 32 && p <= 8) v = make_thread_variant<32, 8, false>();
     else return false;
     return true;
 }
@@ -127,13 +144,13 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+    if (v.smem > 48 * 1024) CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, 32, v.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.block, v.smem));
     if (per_sm < 1) return fail(LAD_E_CUDA, "locus kernel does not fit on an SM (smem %zu)", v.smem);
-    int64_t want = (B + 31) / 32;
+    int64_t want = (B + v.slots_per_block - 1) / v.slots_per_block;
     int64_t grid = std::min<int64_t>(want, (int64_t)g_num_sms * per_sm);
-    int64_t slots = grid * 32;
+    int64_t slots = grid * v.slots_per_block;
 
     lad::LocusArgs A;
     memset(&A, 0, sizeof A);
@@ -166,7 +183,7 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
     A.counter = (unsigned long long *)buf;
     A.seen = A.seen_cap ? (double *)(buf + 256) : nullptr;
     CK(cudaMemsetAsync(buf, 0, 256, st));
-    v.fn<<<(unsigned)grid, 32, v.smem, st>>>(A);
+    v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
     cudaError_t le = cudaGetLastError();
     cudaFreeAsync(buf, st);
     if (le != cudaSuccess) return fail(LAD_E_CUDA, "locus kernel launch: %s", cudaGetErrorString(le));
@@ -174,6 +191,13 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
 }
 
 }  // namespace
+
+extern "C" int lad_set_kernel_policy(int32_t policy)
+{
+    if (policy < LAD_KERNEL_AUTO || policy > LAD_KERNEL_WARP) return fail(LAD_E_INVALID, "unknown kernel policy %d", policy);
+    g_kernel_policy = policy;
+    return LAD_OK;
+}
 
 extern "C" int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
                                    int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
@@ -209,7 +233,9 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
     cudaStream_t st = (cudaStream_t)stream;
     if (B <= 0) return B == 0 ? LAD_OK : fail(LAD_E_INVALID, "B < 0");
     size_t bx = (size_t)B * n * p * 8, by = (size_t)B * n * 8, bl = (size_t)B * 8, bb = (size_t)B * p * 8;
-    size_t total = bx + by + bl + bb + B * 8 + B * 4 * 2 + B * 2 + B * 4 + B * 8 + 1024;
+    auto rup = [](size_t s) { return (s + 255) & ~(size_t)255; };
+    size_t total = rup(bx) + rup(by) + rup(bl) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) + 2 * rup(B) + rup(B * 4) +
+                   rup(B * 8);
     char *d = nullptr;
     CK(cudaMallocAsync((void **)&d, total, st));
     char *q = d;

@@ -87,11 +87,11 @@ def _validate_host(X, y, lam):
         raise InvalidInputError(f"need m >= 1 and d >= 1, got {n} x {p}")
     if y.shape != (B, n):
         raise DimensionMismatchError(f"y has shape {y.shape}, expected {(B, n)}")
-    lam = np.ascontiguousarray(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)))
+    lam = np.array(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)), dtype=np.float64)
     return X, y, lam
 
 
-def _validate_device(X, y, lam):
+def _validate_device(X, y, lam, nlam=None):
     import torch
 
     if X.dtype != torch.float64 or y.dtype != torch.float64:
@@ -101,9 +101,10 @@ def _validate_device(X, y, lam):
     B, n, p = X.shape
     if tuple(y.shape) != (B, n):
         raise DimensionMismatchError(f"y has shape {tuple(y.shape)}, expected {(B, n)}")
+    nl = B if nlam is None else nlam
     if not torch.is_tensor(lam):
-        lam = torch.full((B,), float(lam), dtype=torch.float64, device=X.device)
-    lam = lam.to(torch.float64).expand(B).contiguous()
+        lam = torch.full((nl,), float(lam), dtype=torch.float64, device=X.device)
+    lam = lam.to(device=X.device, dtype=torch.float64).reshape(-1).expand(nl).contiguous()
     return X.contiguous(), y.contiguous(), lam
 
 
@@ -116,13 +117,13 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
     if _is_torch(X):
         import torch
 
-        X, y, lam = _validate_device(X, y, lam)
-        Bd, n, p = X.shape
-        B = lam.shape[0]
         if data_index is not None:
             data_index = data_index.to(device=X.device, dtype=torch.int64).contiguous()
-            B = data_index.shape[0]
-            lam = lam.expand(B).contiguous() if lam.shape[0] == 1 else lam
+            if data_index.numel() and (int(data_index.min()) < 0 or int(data_index.max()) >= X.shape[0]):
+                raise InvalidInputError("data_index out of range")
+        X, y, lam = _validate_device(X, y, lam, None if data_index is None else data_index.shape[0])
+        Bd, n, p = X.shape
+        B = lam.shape[0]
         prm = locus_params(cfg, lambda_floor, p)
         dev = X.device
         beta = torch.empty((B, p), dtype=torch.float64, device=dev)
@@ -179,7 +180,7 @@ def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=N
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
@@ -228,7 +229,7 @@ def solve_brute_batched(X, y, lam, max_variables: int = 6, max_candidates: int =
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
@@ -254,7 +255,7 @@ def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(a).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
         bt = torch.from_numpy(np.ascontiguousarray(beta, dtype=np.float64)).to(dev)
     else:
         Xt, yt, lt = _validate_device(X, y, lam)

@@ -245,3 +245,37 @@ def test_device_generated_subsets_match_host_combinations():
         Xs, Ys = G.subsets(X0, Y0, 25, k, 1)
         rows = list(itertools.combinations(range(30), 25))[k]
         assert torch.equal(Xs[0], X0[list(rows)]) and torch.equal(Ys[0], Y0[list(rows)])
+
+
+@pytest.mark.parametrize("policy", ["thread", "warp"])
+def test_both_kernel_mappings_bit_exact(policy):
+    """The thread-per-problem and warp-per-problem kernels both reproduce the reference."""
+    from paper_2510_15649_b200 import _lib
+
+    _lib.set_kernel_policy(_lib.KERNEL_THREAD if policy == "thread" else _lib.KERNEL_WARP)
+    try:
+        g = load_golden("acceptance")
+        for v in ("ternary", "quadrature"):
+            _assert_exact(_locus_groups(g, v), g, v)
+        for name, v in (("cfg0", "ternary"), ("cfg1", "quadrature"), ("cfg3", "quadrature"), ("cfg4", "ternary")):
+            g = load_golden(name)
+            idx = np.arange(0, len(g["lam"]), 4)
+            r = lad.solve_locus_batched(g["x"][idx], g["y"][idx], g["lam"][idx], lad.LocusConfig(outer_search=v))
+            sub = {k: (g[k][idx] if g[k].shape[:1] == g["lam"].shape else g[k]) for k in g}
+            rr = dict(beta=r.beta, objective=r.objective, iterations=r.iterations, objective_evals=r.objective_evals,
+                      converged=r.converged, D=r.descents, S=r.steps)
+            _assert_exact(rr, sub, v)
+        g = load_golden("params")
+        for i in range(len(g["lam"])):
+            m, d = int(g["m"][i]), int(g["d"][i])
+            cfg = lad.LocusConfig(
+                outer_search=("ternary", "quadrature")[int(g["outer_search"][i])],
+                outer_axis=None if g["outer_axis"][i] < 0 else int(g["outer_axis"][i]),
+                initial_bracket=lad.Bracket(*g["bracket"][i]) if g["has_bracket"][i] else None,
+                outer_probes=int(g["outer_probes"][i]), outer_tolerance=float(g["outer_tolerance"][i]),
+                outer_max_iterations=int(g["outer_max_iterations"][i]),
+                inner=lad.CcdConfig(max_sweeps=int(g["inner_sweeps"][i]), sweep_tolerance=float(g["inner_tol"][i])))
+            r = lad.solve_locus_batched(g["x"][i, :m, :d][None], g["y"][i, :m][None], np.array([g["lam"][i]]), cfg)
+            assert r.objective[0] == g["objective"][i] and r.steps[0] == g["S"][i], (policy, i)
+    finally:
+        _lib.set_kernel_policy(_lib.KERNEL_AUTO)
