@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark: LAD-LASSO solves/sec (n=30, p=5, fp64) on B200 -- BASELINE.json's metric.
+
+Workload (BASELINE.json configs[2], the largest n=30/p=5 configuration): the
+lambda path -- 2^20 datasets generated as config 0, each solved at a 16-point
+log-spaced lambda grid 1e-2..1e1 (cold solves: the reference has no warm-start
+knob).  One bench *step* = one block of datasets (default 2^14)
+x all 16 lambdas = 262,144 solves per GPU; the whole config is 64 such steps.
+Weak scaling: rank r of N solves block (step * N + r).
+
+Timing: per-step CUDA events on the launching stream, L2 flushed (256 MiB
+memset) between steps outside the events, barrier + synchronize around the
+timed region, max over ranks.  ``e2e`` repeats the workload through the
+host-buffer C ABI call (pinned host inputs, H2D + solve + D2H inside the
+timed region).  ``cpu_baseline`` is the CPU oracle (a C restatement of the
+reference's solve_locus, oracle/) on a bounded sample of the same problems,
+all host threads.  ``--impl reference`` times that same CPU path as the
+reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LAD-LASSO solves/sec (n=30,p=5 fp64) at 1/2/4/8 B200; % of roofline"
+N_ROWS, N_FEAT = 30, 5
+LAMBDA_GRID = 10.0 ** np.linspace(-2.0, 1.0, 16)
+TOTAL_DATASETS = 1 << 20
+SEED = 15649 + 2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--block", type=int, default=1 << 14, help="datasets per step per GPU (x16 lambdas)")
+    ap.add_argument("--variant", choices=["ternary", "quadrature"], default="ternary")
+    ap.add_argument("--cpu-sample", type=int, default=64, help="datasets (x16 lambdas) in the CPU baseline sample")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def flops_per_solve(steps, descents, n=N_ROWS, p=N_FEAT):
+    """Algorithmic FP64 flops: S*(8n+4) + D*(4np+4n+4p)."""
+    return steps * (8 * n + 4) + descents * (4 * n * p + 4 * n + 4 * p)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        loaded = [r for r in rows if (num(r[7]) or 0) > 0] or rows
+        sm = [num(r[0]) for r in loaded if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": num(rows[0][1]),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max((num(r[2]) or 0) for r in rows)}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_cpu_sample(X, Y, datasets, variant):
+    """Oracle (CPU restatement of the reference) on datasets x 16 lambdas, all host threads."""
+    from oracle import oracle as O
+
+    O.build()
+    Xs = np.repeat(X[:datasets], 16, axis=0)
+    Ys = np.repeat(Y[:datasets], 16, axis=0)
+    L = np.tile(LAMBDA_GRID, datasets)
+    nth = cpu_threads()
+    t0 = time.perf_counter()
+    r = O.solve_locus_batch(Xs, Ys, L, nthreads=nth, outer_search=variant)
+    dt = time.perf_counter() - t0
+    return r, dt, nth, Xs.shape[0]
+
+
+def run_reference(a, rank, world):
+    """Reference arm: the CPU path (oracle port of solve_locus) on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (device generator provides the identical problem bytes)
+    from paper_2510_15649_b200 import generate as G
+
+    per_step = max(1, min(a.cpu_sample, 16))
+    times, solves = [], 0
+    for s in range(a.warmup + a.steps):
+        Xd, Yd, _ = G.generate(2, per_step, seed=SEED, first=(s * a.block) % TOTAL_DATASETS)
+        X, Y = Xd.cpu().numpy(), Yd.cpu().numpy()
+        _, dt, nth, ns = run_cpu_sample(X, Y, per_step, a.variant)
+        if s >= a.warmup:
+            times.append(dt)
+            solves += ns
+    total = sum(times)
+    value = solves / total
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "solves/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox generator, BASELINE config 2 distributions)",
+            "config": {"workload": "config2_lambda_path", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
+                       "variant": a.variant, "solves_per_step": per_step * 16},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": nth, "kind": "port",
+                             "sample": f"{per_step} config-2 datasets x 16 lambdas per step"},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2510_15649_b200 as lad
+    from paper_2510_15649_b200 import generate as G
+    from paper_2510_15649_b200.solver import fp64_peak_tflops
+
+    blk = a.block
+    cfg = lad.LocusConfig(outer_search=a.variant)
+    nsteps = a.warmup + a.steps
+    # device-resident inputs for every step this rank will run (generated before timing)
+    blocks = []
+    for s in range(nsteps):
+        g = s * world + rank
+        first = (g * blk) % TOTAL_DATASETS
+        X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
+        blocks.append((first, X, Y))
+    data_index = torch.arange(blk, device=dev, dtype=torch.int64).repeat_interleave(16)
+    lam = torch.tensor(LAMBDA_GRID, device=dev, dtype=torch.float64).repeat(blk)
+    solves_per_step = blk * 16
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    peak = fp64_peak_tflops()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(a.warmup):
+        lad.solve_locus_batched(blocks[s][1], blocks[s][2], lam, cfg, data_index=data_index)
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    results = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(a.steps):
+            _, X, Y = blocks[a.warmup + k]
+            flush.zero_()
+            evs[k][0].record(stream)
+            r = lad.solve_locus_batched(X, Y, lam, cfg, data_index=data_index)
+            evs[k][1].record(stream)
+            results.append(r)
+        barrier()
+    clocks = clk.summary()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    elapsed = sum(step_ms) / 1e3
+    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_max = float(t.item())
+    value = world * a.steps * solves_per_step / elapsed_max
+    # algorithmic flops of the timed launches (exact per-problem counters)
+    S = sum(float(r.steps.double().sum()) for r in results)
+    D = sum(float(r.descents.double().sum()) for r in results)
+    fl = flops_per_solve(S, D)
+    achieved_tflops = fl / elapsed / 1e12
+    status_ok = all(bool((r.status == 0).all()) for r in results)
+    conv_frac = float(np.mean([float(r.converged.float().mean()) for r in results]))
+
+    # ---- end to end through the host-buffer C ABI (pinned host memory, copies inside)
+    e2e_steps = a.e2e_steps if a.e2e_steps is not None else min(a.steps, 3)
+    host = []
+    for k in range(e2e_steps):
+        _, X, Y = blocks[a.warmup + k]
+        hx = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
+        hy = torch.empty(Y.shape, dtype=torch.float64, pin_memory=True)
+        hx.copy_(X)
+        hy.copy_(Y)
+        host.append((hx.numpy(), hy.numpy()))
+    hidx = torch.empty(data_index.shape, dtype=torch.int64, pin_memory=True)
+    hidx.copy_(data_index)
+    hlam = torch.empty(lam.shape, dtype=torch.float64, pin_memory=True)
+    hlam.copy_(lam)
+    hidx_np, hlam_np = hidx.numpy(), hlam.numpy()
+    barrier()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        r = lad.solve_locus_batched(host[k][0], host[k][1], hlam_np, cfg, data_index=hidx_np)
+    barrier()
+    e2e_elapsed = time.perf_counter() - t0
+    te = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * e2e_steps * solves_per_step / float(te.item())
+    h2d = host[0][0].nbytes + host[0][1].nbytes + hlam_np.nbytes + hidx_np.nbytes
+    d2h = solves_per_step * (N_FEAT * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        first, X, Y = blocks[a.warmup]
+        ns = min(a.cpu_sample, blk)
+        Xh, Yh = X[:ns].cpu().numpy(), Y[:ns].cpu().numpy()
+        ro, dt, nth, nsol = run_cpu_sample(Xh, Yh, ns, a.variant)
+        cpu = {"value": nsol / dt, "unit": "solves/s", "cores": nth, "kind": "port",
+               "sample": f"{ns} config-2 datasets x 16 lambdas ({nsol} solves) of the first timed step, "
+                         f"CPU oracle (C restatement of solve_locus) on {nth} threads, {dt:.1f} s"}
+        g = results[0]
+        gb = g.beta[: nsol].cpu().numpy()
+        go = g.objective[: nsol].cpu().numpy()
+        gs = g.steps[: nsol].cpu().numpy()
+        exact = int(np.sum(np.all(gb == ro["beta"], axis=1) & (go == ro["objective"]) & (gs == ro["steps"])))
+        rel = np.abs(go - ro["objective"]) / np.abs(ro["objective"])
+        parity = {"sample": nsol, "bit_exact": exact, "obj_within_1e-9": int(np.sum(rel <= 1e-9))}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": elapsed_max * 1e3 / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox generator, BASELINE config 2 distributions: X~N(0,1), "
+                    "2 nonzeros +-U[1,3], Laplace(0,0.5), 10% rows +-10)",
+            "config": {"workload": "config2_lambda_path", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
+                       "datasets_per_step_per_gpu": blk, "solves_per_step_per_gpu": solves_per_step,
+                       "variant": a.variant, "parallelism": f"shard{world} (independent problems, no collective)",
+                       "kernel": "warp-per-problem sm_100a", "l2": "flushed between steps (256 MiB memset)"},
+            "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / peak if peak else None, "traffic": None,
+                         "peak_source": "measured DFMA loop on this GPU (lad_fp64_peak_tflops); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "flops_per_solve": fl / (a.steps * solves_per_step),
+                         "coord_steps_per_solve": S / (a.steps * solves_per_step),
+                         "descents_per_solve": D / (a.steps * solves_per_step)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+            "gpu_launches": a.steps,
+            "clocks": clocks,
+            "status_ok": status_ok,
+            "converged_frac": conv_frac,
+            "parity_sample": parity,
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,9 +85,11 @@ int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, con
 
 /* Same with HOST pointers for inputs and outputs (pinned or pageable); the
  * host<->device copies run inside the call on `stream`, which is synchronized
- * before returning.  out fields are host pointers. */
-int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
-                             const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+ * before returning.  out fields are host pointers.  X (Bd, n, p), Y (Bd, n);
+ * data_index (B,) host array or NULL (then Bd == B). */
+int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
+                             int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                             const lad_locus_out *out, void *stream);
 
 /* Batched ccd_descend from `start` (B, p); frozen (B,) axis or -1 (NULL = none). */
 int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
@@ -100,6 +102,10 @@ int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int
 int lad_brute_solve_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
                         int32_t max_variables, int64_t max_candidates, double lambda_floor, double *beta,
                         double *objective, int64_t *vertices, void *stream);
+
+/* Roofline denominator: measured dense FP64 FMA throughput of the current
+ * device (TFLOP/s, 2 flops per DFMA), timed with CUDA events on `stream`. */
+int lad_fp64_peak_tflops(double *tflops, void *stream);
 
 /* evaluate_objective for (B, p) coefficient vectors. */
 int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,

@@ -20,6 +20,7 @@ SYMBOLS = (
     "lad_locus_solve_host_f64",
     "lad_ccd_descend_f64",
     "lad_brute_solve_f64",
+    "lad_fp64_peak_tflops",
     "lad_objective_f64",
     "lad_generate_f64",
     "lad_subsets_f64",
@@ -99,7 +100,9 @@ def load(build_if_missing: bool = False):
     L.lad_default_params.restype = None
     L.lad_set_kernel_policy.argtypes = [i32]
     L.lad_locus_solve_f64.argtypes = [vp, vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
-    L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
+    L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams),
+                                           C.POINTER(LocusOut), vp]
+    L.lad_fp64_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
     L.lad_ccd_descend_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, dbl, i32, dbl, C.POINTER(LocusOut), vp]
     L.lad_brute_solve_f64.argtypes = [vp, vp, vp, i64, i32, i32, i32, i64, dbl, vp, vp, vp, vp]
     L.lad_objective_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, dbl, vp, vp]

@@ -226,25 +226,29 @@ extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const doubl
                      sweep_tolerance, max_sweeps);
 }
 
-extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
-                                        int32_t p, const lad_locus_params *prm, const lad_locus_out *out,
-                                        void *stream)
+extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam,
+                                        const int64_t *data_index, int64_t Bd, int64_t B, int32_t n, int32_t p,
+                                        const lad_locus_params *prm, const lad_locus_out *out, void *stream)
 {
     cudaStream_t st = (cudaStream_t)stream;
-    if (B <= 0) return B == 0 ? LAD_OK : fail(LAD_E_INVALID, "B < 0");
-    size_t bx = (size_t)B * n * p * 8, by = (size_t)B * n * 8, bl = (size_t)B * 8, bb = (size_t)B * p * 8;
+    if (B < 0 || Bd < 0) return fail(LAD_E_INVALID, "B < 0");
+    if (!data_index && Bd != B) return fail(LAD_E_INVALID, "Bd must equal B without data_index");
+    if (B == 0) return LAD_OK;
     auto rup = [](size_t s) { return (s + 255) & ~(size_t)255; };
-    size_t total = rup(bx) + rup(by) + rup(bl) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) + 2 * rup(B) + rup(B * 4) +
-                   rup(B * 8);
+    size_t bx = (size_t)Bd * n * p * 8, by = (size_t)Bd * n * 8, bl = (size_t)B * 8, bb = (size_t)B * p * 8;
+    size_t bi = data_index ? (size_t)B * 8 : 0;
+    size_t total = rup(bx) + rup(by) + rup(bl) + rup(bi) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) + 2 * rup(B) +
+                   rup(B * 4) + rup(B * 8);
     char *d = nullptr;
     CK(cudaMallocAsync((void **)&d, total, st));
     char *q = d;
     auto take = [&](size_t sz) {
         char *r = q;
-        q += (sz + 255) & ~(size_t)255;
+        q += rup(sz);
         return r;
     };
     double *dX = (double *)take(bx), *dY = (double *)take(by), *dL = (double *)take(bl);
+    int64_t *dI = data_index ? (int64_t *)take(bi) : nullptr;
     lad_locus_out dout;
     dout.beta = (double *)take(bb);
     dout.objective = (double *)take(B * 8);
@@ -254,23 +258,72 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
     dout.status = (uint8_t *)take(B);
     dout.descents = out->descents ? (int32_t *)take(B * 4) : nullptr;
     dout.steps = out->steps ? (int64_t *)take(B * 8) : nullptr;
-    CK(cudaMemcpyAsync(dX, X, bx, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st));
-    int rc = lad_locus_solve_f64(dX, dY, dL, nullptr, B, n, p, prm, &dout, stream);
-    if (rc == LAD_OK) {
-        CK(cudaMemcpyAsync(out->beta, dout.beta, bb, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(out->objective, dout.objective, B * 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(out->iterations, dout.iterations, B * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(out->objective_evals, dout.objective_evals, B * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(out->converged, dout.converged, B, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(out->status, dout.status, B, cudaMemcpyDeviceToHost, st));
-        if (out->descents) CK(cudaMemcpyAsync(out->descents, dout.descents, B * 4, cudaMemcpyDeviceToHost, st));
-        if (out->steps) CK(cudaMemcpyAsync(out->steps, dout.steps, B * 8, cudaMemcpyDeviceToHost, st));
+    int rc = LAD_OK;
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dX, X, bx, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && dI) e = cudaMemcpyAsync(dI, data_index, bi, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) rc = lad_locus_solve_f64(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
+    if (e == cudaSuccess && rc == LAD_OK) {
+        struct { void *h; const void *d; size_t s; } cp[] = {
+            {out->beta, dout.beta, bb}, {out->objective, dout.objective, (size_t)B * 8},
+            {out->iterations, dout.iterations, (size_t)B * 4}, {out->objective_evals, dout.objective_evals, (size_t)B * 4},
+            {out->converged, dout.converged, (size_t)B}, {out->status, dout.status, (size_t)B},
+            {out->descents, dout.descents, (size_t)B * 4}, {out->steps, dout.steps, (size_t)B * 8}};
+        for (auto &c : cp)
+            if (c.h && c.d && e == cudaSuccess) e = cudaMemcpyAsync(c.h, c.d, c.s, cudaMemcpyDeviceToHost, st);
     }
     cudaFreeAsync(d, st);
-    CK(cudaStreamSynchronize(st));
-    return rc;
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(LAD_E_CUDA, "host solve copies: %s", cudaGetErrorString(e));
+    if (rc != LAD_OK) return rc;
+    if (se != cudaSuccess) return fail(LAD_E_CUDA, "host solve: %s", cudaGetErrorString(se));
+    return LAD_OK;
+}
+
+namespace {
+__global__ void fp64_peak_kernel(double *out, int iters)
+{
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9, a4 = a0 + 4e-9, a5 = a0 + 5e-9,
+           a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+        a0 = __fma_rn(a0, m, c); a1 = __fma_rn(a1, m, c); a2 = __fma_rn(a2, m, c); a3 = __fma_rn(a3, m, c);
+        a4 = __fma_rn(a4, m, c); a5 = __fma_rn(a5, m, c); a6 = __fma_rn(a6, m, c); a7 = __fma_rn(a7, m, c);
+    }
+    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.0) out[0] = s;  // keep the chain alive
+}
+}  // namespace
+
+extern "C" int lad_fp64_peak_tflops(double *tflops, void *stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    if (g_num_sms == 0) {
+        int dev;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int block = 256, blocks = g_num_sms * 8, iters = 1 << 14;
+    double *dout = nullptr;
+    CK(cudaMallocAsync((void **)&dout, 8, st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    fp64_peak_kernel<<<blocks, block, 0, st>>>(dout, iters);  // warm-up
+    CK(cudaEventRecord(e0, st));
+    fp64_peak_kernel<<<blocks, block, 0, st>>>(dout, iters);
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(dout, st);
+    double flops = 2.0 * 8.0 * iters * (double)block * blocks;
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return LAD_OK;
 }
 
 namespace {

@@ -143,10 +143,16 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
                                      C.byref(prm), C.byref(out), s))
         res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
     else:
+        X, y, lam0 = _validate_host(X, y, 0.0)
+        Bd, n, p = X.shape
         if data_index is not None:
-            raise InvalidInputError("data_index is supported for device tensors only")
-        X, y, lam = _validate_host(X, y, lam)
-        B, n, p = X.shape
+            data_index = np.ascontiguousarray(data_index, dtype=np.int64)
+            if data_index.size and (data_index.min() < 0 or data_index.max() >= Bd):
+                raise InvalidInputError("data_index out of range")
+            B = data_index.shape[0]
+        else:
+            B = Bd
+        lam = np.array(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)), dtype=np.float64)
         prm = locus_params(cfg, lambda_floor, p)
         beta = np.empty((B, p))
         obj = np.empty(B)
@@ -158,8 +164,9 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
         stp = np.empty(B, np.int64)
         out = _lib.LocusOut(*(a.ctypes.data for a in (beta, obj, it, ev, cv, stt, dsc, stp)))
         t0 = time.perf_counter()
-        _check(L.lad_locus_solve_host_f64(X.ctypes.data, y.ctypes.data, lam.ctypes.data, B, n, p, C.byref(prm),
-                                          C.byref(out), stream))
+        _check(L.lad_locus_solve_host_f64(X.ctypes.data, y.ctypes.data, lam.ctypes.data,
+                                          None if data_index is None else data_index.ctypes.data, Bd, B, n, p,
+                                          C.byref(prm), C.byref(out), stream))
         res = BatchedSolveResult(beta, obj, it, ev, cv.astype(bool), stt, dsc, stp, solver_id,
                                  time.perf_counter() - t0)
     if strict:
@@ -244,6 +251,15 @@ def solve_brute_batched(X, y, lam, max_variables: int = 6, max_candidates: int =
     if host:
         return beta.cpu().numpy(), obj.cpu().numpy(), nv.cpu().numpy()
     return beta, obj, nv
+
+
+def fp64_peak_tflops() -> float:
+    """Measured dense DFMA throughput of the current device (roofline denominator)."""
+    import torch
+
+    v = C.c_double()
+    _check(_lib.load().lad_fp64_peak_tflops(C.byref(v), torch.cuda.current_stream().cuda_stream))
+    return v.value
 
 
 def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT_LAMBDA_FLOOR):
