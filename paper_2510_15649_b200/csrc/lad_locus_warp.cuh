@@ -30,6 +30,8 @@ struct WarpShared {
     double Y[32];
     double B[PMAX];       // beta of the running descent (warp-uniform)
     double sa[32], sw[32], sz[32];
+    double2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
+    int perm[PMAX][32];   // per axis: sorted position -> element of the last sort
 };
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULLMASK, v, src); }
@@ -191,53 +193,164 @@ struct WarpAccess {
     }
 };
 
-// One exact coordinate step on axis j (ccd.py:160-193), all lanes.
+__device__ __forceinline__ uint32_t bitonic_inv_mask(int lane)
+{
+    uint32_t m = 0;
+    int s = 0;
+    for (int k = 2; k <= 32; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1, ++s) {
+            bool up = (lane & k) == 0;
+            bool lower = (lane & j) == 0;
+            if (lower != up) m |= 1u << s;
+        }
+    return m;
+}
+
+// Ascending bitonic sort of (key, idx) over 32 lanes, lexicographic, with
+// the per-lane direction bits precomputed.
+__device__ __forceinline__ void bitonic32m(double &key, int &idx, uint32_t inv_mask)
+{
+    int s = 0;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1, ++s) {
+            double pk = shfl_xor_d(key, j);
+            int pi = __shfl_xor_sync(FULLMASK, idx, j);
+            bool plt = (pk < key) | ((pk == key) & (pi < idx));
+            bool take = plt != (((inv_mask >> s) & 1u) != 0u);
+            key = take ? pk : key;
+            idx = take ? pi : idx;
+        }
+    }
+}
+
+// (key, idx) ascending across lanes 0..31 (lexicographic)?
+__device__ __forceinline__ bool warp_is_sorted(double key, int idx, int lane)
+{
+    const double nk = shfl_down_d(key, 1);
+    const int ni = __shfl_down_sync(FULLMASK, idx, 1);
+    const bool ok = (lane == 31) || (key < nk) || ((key == nk) && (idx < ni));
+    return __all_sync(FULLMASK, ok);
+}
+
+// One odd-even transposition phase: pairs (2i, 2i+1) for phase 0, (2i+1, 2i+2)
+// for phase 1; the lower lane of a pair keeps the smaller (key, idx).
+__device__ __forceinline__ void oddeven_phase(double &key, int &idx, int lane, int phase)
+{
+    const bool odd = lane & 1;
+    const bool lower = (phase == 0) ? !odd : odd;
+    int partner = lower ? lane + 1 : lane - 1;
+    const bool paired = partner >= 0 && partner < 32;
+    partner = paired ? partner : lane;
+    const double pk = shfl_d(key, partner);
+    const int pi = __shfl_sync(FULLMASK, idx, partner);
+    const bool plt = (pk < key) | ((pk == key) & (pi < idx));
+    const bool take = paired && (lower ? plt : !plt);
+    key = take ? pk : key;
+    idx = take ? pi : idx;
+}
+
+// numpy's sequential cumsum in sorted order, recomputed exactly (rare path:
+// only when the parallel scan leaves a comparison within 1e-13 of a tie).
+__device__ __forceinline__ void exact_cumsum_decision(double ws, int lane, int cnt, int &k, double &ck, double &total,
+                                                   double &half)
+{
+    double ce = 0.0;
+    for (int i = 0; i < 32; ++i) {
+        double wi = shfl_d(ws, i);
+        if (i <= lane) ce = dadd(ce, wi);
+    }
+    total = shfl_d(ce, cnt - 1);
+    half = dmul(0.5, total);
+    k = __popc(__ballot_sync(FULLMASK, lane < cnt && ce < half));
+    ck = shfl_d(ce, k < cnt ? k : cnt - 1);
+}
+
+// _AxisWorkspace for a column with zero entries (ccd.py:94-110, :167-169,
+// :178-179): nonzero rows compacted to lanes 0..k-1 in row order, the zero
+// rows' |r| summed with numpy's pairwise order.  Rare path.
 template <int PMAX>
-__device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, int n, int p, int j, double lam,
-                                          bool col_sparse, double &r, double &f_cur, double &sum_abs_b)
+__device__ __forceinline__ void sparse_column(WarpShared<PMAX> *W, int lane, int n, double r, double xij, double bj,
+                                           double lam, double &loc, double &w, int &cnt, double &zsum)
 {
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
     const bool row = lane < n;
-    const double xij = row ? W->X[lane * p + j] : 0.0;
+    const bool nz = row && xij != 0.0;
+    const unsigned nzm = __ballot_sync(FULLMASK, nz);
+    const unsigned zm = __ballot_sync(FULLMASK, row && xij == 0.0);
+    const unsigned lt = (1u << lane) - 1u;
+    const int k = __popc(nzm), z = __popc(zm);
+    const bool dense = (k == n);
+    __syncwarp();
+    if (nz) {
+        W->sa[__popc(nzm & lt)] = dense ? dadd(ddiv(r, xij), bj) : ddiv(dadd(r, dmul(xij, bj)), xij);
+        W->sw[__popc(nzm & lt)] = fabs(xij);
+    }
+    if (row && xij == 0.0) W->sz[__popc(zm & lt)] = fabs(r);
+    __syncwarp();
+    loc = lane < k ? W->sa[lane] : (lane == k ? 0.0 : INF);
+    w = lane < k ? W->sw[lane] : (lane == k ? lam : 0.0);
+    const double zv = lane < z ? W->sz[lane] : 0.0;
+    __syncwarp();
+    zsum = z > 0 ? warp_np_sum(zv, z, lane) : 0.0;
+    cnt = k + 1;
+}
+
+// One exact coordinate step on axis j (ccd.py:160-193), all lanes in lock-step.
+// NC > 0: compile-time row count (config shapes); NC == 0: runtime n_rt.
+template <int PMAX, int NC>
+__device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_t inv_mask, const double *xrow,
+                                          int n_rt, int j, double lam, bool col_sparse, double &r, double &f_cur,
+                                          double &sum_abs_b, uint32_t &perm_valid)
+{
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const int n = NC > 0 ? NC : n_rt;
+    const bool row = lane < n;
+    const double xij = xrow[j];  // lanes >= n read a stale in-bounds slot, never used
     const double bj = W->B[j];
     double loc, w, zsum = 0.0;
     int cnt;
-    bool have_zero = false;
     if (!col_sparse) {
-        loc = row ? dadd(ddiv(r, xij), bj) : (lane == n ? 0.0 : INF);  // np.divide then += b[j]
+        const double q = ddiv(row ? r : 0.0, row ? xij : 1.0);  // np.divide then += b[j] (ccd.py:165-166)
+        loc = row ? dadd(q, bj) : (lane == n ? 0.0 : INF);
         w = row ? fabs(xij) : (lane == n ? lam : 0.0);
         cnt = n + 1;
     } else {
-        // _AxisWorkspace with zero rows (ccd.py:94-110, :167-169, :178-179)
-        const bool nz = row && xij != 0.0;
-        const unsigned nzm = __ballot_sync(FULLMASK, nz);
-        const unsigned zm = __ballot_sync(FULLMASK, row && xij == 0.0);
-        const unsigned lt = (1u << lane) - 1u;
-        const int k = __popc(nzm), z = __popc(zm);
-        const bool dense = (k == n);
-        if (nz) {
-            W->sa[__popc(nzm & lt)] = dense ? dadd(ddiv(r, xij), bj) : ddiv(dadd(r, dmul(xij, bj)), xij);
-            W->sw[__popc(nzm & lt)] = fabs(xij);
-        }
-        if (row && xij == 0.0) W->sz[__popc(zm & lt)] = fabs(r);
-        __syncwarp();
-        loc = lane < k ? W->sa[lane] : (lane == k ? 0.0 : INF);
-        w = lane < k ? W->sw[lane] : (lane == k ? lam : 0.0);
-        double zv = lane < z ? W->sz[lane] : 0.0;
-        __syncwarp();
-        have_zero = z > 0;
-        zsum = have_zero ? warp_np_sum(zv, z, lane) : 0.0;
-        cnt = k + 1;
+        sparse_column<PMAX>(W, lane, n, r, xij, bj, lam, loc, w, cnt, zsum);
     }
-    // ---- weighted median (ccd.py:81-91)
-    double key = loc;
-    int idx = lane;
-    bitonic32(key, idx, lane);
+    // ---- weighted median (ccd.py:81-91): stable order by (location, index).
+    // The order is unique, so if this axis' permutation from the previous
+    // sweep is still sorted under the new locations it is the answer; the
+    // 15-stage network runs only when the check fails.
+    double key;
+    int idx;
+    bool sorted = false;
+    if (!col_sparse && ((perm_valid >> j) & 1u)) {
+        idx = W->perm[j][lane];
+        key = shfl_d(loc, idx);
+        sorted = warp_is_sorted(key, idx, lane);
+        // nearly sorted (typical between sweeps): odd-even transposition rounds
+#pragma unroll 1
+        for (int round = 0; round < 2 && !sorted; ++round) {
+            oddeven_phase(key, idx, lane, 0);
+            oddeven_phase(key, idx, lane, 1);
+            sorted = warp_is_sorted(key, idx, lane);
+        }
+        if (sorted) W->perm[j][lane] = idx;
+    }
+    if (!sorted) {
+        key = loc;
+        idx = lane;
+        bitonic32m(key, idx, inv_mask);
+        if (!col_sparse) W->perm[j][lane] = idx;
+    }
+    perm_valid |= 1u << j;
     const double ws = shfl_d(w, idx);
     double c = ws;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        double t = __shfl_up_sync(FULLMASK, c, d);
+        const double t = __shfl_up_sync(FULLMASK, c, d);
         if (lane >= d) c = dadd(c, t);
     }
     const bool in = lane < cnt;
@@ -245,19 +358,14 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, int n, 
     double half = dmul(0.5, total);
     int k = __popc(__ballot_sync(FULLMASK, in && c < half));
     double ck = shfl_d(c, k < cnt ? k : cnt - 1);
-    const double marg = dmul(1e-13, total);
-    bool risky = __any_sync(FULLMASK, in && fabs(dsub(c, half)) <= marg) ||
-                 fabs(dsub(fabs(dsub(ck, half)), dmul(1e-12, total))) <= marg;
-    if (risky) {  // exact: numpy's sequential cumsum in sorted order
-        double ce = 0.0;
-        for (int i = 0; i < 32; ++i) {
-            double wi = shfl_d(ws, i);
-            if (i <= lane) ce = dadd(ce, wi);
-        }
-        total = shfl_d(ce, cnt - 1);
-        half = dmul(0.5, total);
-        k = __popc(__ballot_sync(FULLMASK, in && ce < half));
-        ck = shfl_d(ce, k < cnt ? k : cnt - 1);
+    {
+        // the parallel scan rounds differently from numpy's sequential cumsum
+        // by at most ~6e-15 * total; every decision below is taken with a
+        // 1e-13 * total margin or recomputed exactly
+        const double marg = dmul(1e-13, total);
+        const bool risky = __any_sync(FULLMASK, in && fabs(dsub(c, half)) <= marg) ||
+                           fabs(dsub(fabs(dsub(ck, half)), dmul(1e-12, total))) <= marg;
+        if (risky) exact_cumsum_decision(ws, lane, cnt, k, ck, total, half);
     }
     const bool tie = (k + 1 < cnt) && fabs(dsub(ck, half)) <= dmul(1e-12, total);
     const int ks = k < cnt ? k : cnt - 1;
@@ -267,18 +375,44 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, int n, 
     // ---- skip / evaluate / accept (ccd.py:172-191)
     if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
     double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
-    if (have_zero) constant = dadd(constant, zsum);
-    const double a = lane < cnt ? fabs(dsub(t_new, loc)) : 0.0;
-    const double dot = warp_blas_ddot<PMAX>(a, lane < cnt ? w : 0.0, cnt, lane, W);
+    if (col_sparse) constant = dadd(constant, zsum);
+    // v_new: |t - loc| @ weights through OpenBLAS ddot's tree (see warp_blas_ddot)
+    const double a = in ? fabs(dsub(t_new, loc)) : 0.0;
+    const double wv = in ? w : 0.0;
+    const int n1 = cnt & -16;
+    const double pr = dmul(a, wv);
+    double dot = 0.0;
+    if (n1 == 16) {
+        const double q4 = shfl_down_d(pr, 4), q8 = shfl_down_d(pr, 8), q12 = shfl_down_d(pr, 12);
+        const double S = dadd(dadd(dadd(pr, q4), q8), q12);
+        const double u = dadd(S, shfl_down_d(S, 2));
+        dot = shfl_d(dadd(u, shfl_down_d(u, 1)), 0);
+    } else if (n1 == 32) {
+        const double A2 = dadd(pr, shfl_down_d(pr, 4));
+        const double a8 = shfl_down_d(A2, 8), a16 = shfl_down_d(A2, 16), a24 = shfl_down_d(A2, 24);
+        const double S = dadd(dadd(dadd(A2, a8), a16), a24);
+        const double u = dadd(S, shfl_down_d(S, 2));
+        dot = shfl_d(dadd(u, shfl_down_d(u, 1)), 0);
+    }
+    if (n1 < cnt) {  // FMA tail in index order, operands as (a, w) pairs from shared memory
+        W->aw[lane] = make_double2(a, wv);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {  // tail length cnt - n1 < 16
+            if (n1 + t < cnt) {
+                const double2 q = W->aw[n1 + t];
+                dot = dfma(q.x, q.y, dot);
+            }
+        }
+        __syncwarp();
+    }
     const double v_new = dadd(constant, dot);
-    if (v_new < f_cur) {
+    if (v_new < f_cur) {  // strict accept
         const double delta = dsub(t_new, bj);
-        if (row) r = dsub(r, dmul(xij, delta));
+        r = row ? dsub(r, dmul(xij, delta)) : r;
         sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
         f_cur = v_new;
-        __syncwarp();
-        if (lane == 0) W->B[j] = t_new;
-        __syncwarp();
+        W->B[j] = t_new;  // every lane stores the same value: no cross-lane hazard
     }
 }
 
@@ -296,9 +430,12 @@ __device__ __forceinline__ double warp_objective(WarpShared<PMAX> *W, int lane, 
 }
 
 // ccd_descend (ccd.py:126-206) for the descent request in C, all lanes.
-template <int PMAX>
-__device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int lane, int n, int p)
+template <int PMAX, int NC>
+__device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
+                                          int p_rt, uint32_t &perm_valid)
 {
+    const int n = NC > 0 ? NC : n_rt;
+    const int p = NC > 0 ? PMAX : p_rt;
     const int frozen = C.req_frozen;
     const double tol = C.req_tol;
     const int max_sweeps = C.req_sweeps;
@@ -311,19 +448,22 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int
         double g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * p + q]; }, [&](int q) { return W->B[q]; });
         r = dsub(W->Y[lane], g);
     }
+    const double *xrow = W->X + lane * p;
     const double sb = np_sum(p, [&](int q) { return fabs(W->B[q]); });
     double f_cur = dadd(warp_np_sum(fabs(r), n, lane), dmul(lam, sb));
     double f_sweep_start = f_cur, sum_abs_b = sb;
     int sweeps = 1, steps = 0, conv = 0;
-    int j = (frozen == 0) ? 1 : 0;
+    const int j0 = (frozen == 0) ? 1 : 0;
+    int j = j0;
     if (j >= p) {
         conv = 1;
     } else {
         for (;;) {
-            warp_step<PMAX>(W, lane, n, p, j, lam, (sparse >> j) & 1u, r, f_cur, sum_abs_b);
+            warp_step<PMAX, NC>(W, lane, inv_mask, xrow, n, j, lam, (sparse >> j) & 1u, r, f_cur, sum_abs_b,
+                                perm_valid);
             ++steps;
             int jn = j + 1;
-            if (jn == frozen) ++jn;
+            jn += (jn == frozen);
             if (jn < p) {
                 j = jn;
                 continue;
@@ -336,9 +476,10 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int
             ++sweeps;
             f_sweep_start = f_cur;
             sum_abs_b = np_sum(p, [&](int q) { return fabs(W->B[q]); });
-            j = (frozen == 0) ? 1 : 0;
+            j = j0;
         }
     }
+    __syncwarp();
     const double obj = warp_objective<PMAX>(W, lane, n, p, lam);
     const int D = C.D;
     const long long S = C.S;
@@ -355,16 +496,21 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int
     __syncwarp();
 }
 
-template <int PMAX>
+// PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
+template <int PMAX, int NC>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK) locus_warp_kernel(LocusArgs A)
 {
     __shared__ WarpShared<PMAX> WS[WARPS_PER_BLOCK];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     WarpShared<PMAX> *W = &WS[wib];
-    const int n = A.n, p = A.p;
+    const int n = NC > 0 ? NC : A.n, p = NC > 0 ? PMAX : A.p;
     const int slot = blockIdx.x * WARPS_PER_BLOCK + wib;
     WarpAccess<PMAX> acc{n, p, lane, W};
+    const uint32_t inv_mask = bitonic_inv_mask(lane);
+    // cached breakpoint orders per axis (validated before every use, so they
+    // may be carried across descents and problems)
+    uint32_t perm_valid = 0;
     Ctl<PMAX> &C = W->C;
     if (lane == 0) C.pc = PC_FETCH;
     __syncwarp();
@@ -372,7 +518,7 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK) locus_warp_kernel(LocusA
         int act = controller<PMAX>(C, A, acc, slot);
         __syncwarp();
         if (act == ACT_EXIT) break;
-        warp_descent<PMAX>(W, C, lane, n, p);
+        warp_descent<PMAX, NC>(W, C, lane, inv_mask, n, p, perm_valid);
     }
 }
 

@@ -77,10 +77,10 @@ Variant make_thread_variant()
     return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double), 32, 32};
 }
 
-template <int P>
+template <int P, int NC>
 Variant make_warp_variant()
 {
-    return Variant{lad::locus_warp_kernel<P>, 31, P, 0, 32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
+    return Variant{lad::locus_warp_kernel<P, NC>, 31, P, 0, 32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
 }
 
 int g_kernel_policy = LAD_KERNEL_AUTO;
@@ -92,9 +92,13 @@ bool pick_variant(int n, int p, Variant &v)
     int policy = g_kernel_policy;
     if (policy == LAD_KERNEL_AUTO) policy = (thread_exact || !warp_ok) ? LAD_KERNEL_THREAD : LAD_KERNEL_WARP;
     if (policy == LAD_KERNEL_WARP && warp_ok) {
-        if (p <= 3) v = make_warp_variant<3>();
-        else if (p <= 5) v = make_warp_variant<5>();
-        else v = make_warp_variant<8>();
+        // compile-time shapes of BASELINE configs 0/2 (30,5), 3 (25,5), 4 (31,8)
+        if (n == 30 && p == 5) v = make_warp_variant<5, 30>();
+        else if (n == 25 && p == 5) v = make_warp_variant<5, 25>();
+        else if (n == 31 && p == 8) v = make_warp_variant<8, 31>();
+        else if (p <= 3) v = make_warp_variant<3, 0>();
+        else if (p <= 5) v = make_warp_variant<5, 0>();
+        else v = make_warp_variant<8, 0>();
         return true;
     }
     if (thread_exact) v = make_thread_variant<10, 2, true>();
