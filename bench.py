@@ -189,6 +189,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     import paper_2510_15649_b200 as lad
     from paper_2510_15649_b200 import generate as G
+    from paper_2510_15649_b200.distributed import block_for_step
     from paper_2510_15649_b200.solver import fp64_peak_tflops
 
     blk = a.block
@@ -197,8 +198,7 @@ def main():
     # device-resident inputs for every step this rank will run (generated before timing)
     blocks = []
     for s in range(nsteps):
-        g = s * world + rank
-        first = (g * blk) % TOTAL_DATASETS
+        first = block_for_step(s, world, rank, TOTAL_DATASETS // blk) * blk
         X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
         blocks.append((first, X, Y))
     data_index = torch.arange(blk, device=dev, dtype=torch.int64).repeat_interleave(16)

@@ -162,3 +162,13 @@ def test_config_shapes_bit_exact(oracle, name, variants):
             beta, obj, nv = oracle.solve_brute(g["x"][i], g["y"][i], max(float(g["lam"][i]), 1e-9))
             assert obj == g["brute_objective"][j] and np.array_equal(beta, g["brute_beta"][j])
             assert nv == g["brute_vertices"][j]
+
+
+def test_numerics_model_matches_live_numpy():
+    """The restated numpy/OpenBLAS orders match this interpreter's numpy (SkylakeX OpenBLAS only)."""
+    from oracle import probe_numerics as P
+
+    if P.openblas_arch() != "SkylakeX":
+        pytest.skip(f"order model measured for OpenBLAS SkylakeX kernels, host uses {P.openblas_arch()}")
+    res = P.check(trials=10)
+    assert all(v == 0 for v in res.values()), res
