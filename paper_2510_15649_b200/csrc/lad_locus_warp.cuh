@@ -297,40 +297,28 @@ __device__ __forceinline__ void sparse_column(WarpShared<PMAX> *W, int lane, int
     cnt = k + 1;
 }
 
-// One exact coordinate step on axis j (ccd.py:160-193), all lanes in lock-step.
-// NC > 0: compile-time row count (config shapes); NC == 0: runtime n_rt.
-template <int PMAX, int NC>
-__device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_t inv_mask, const double *xrow,
-                                          int n_rt, int j, double lam, bool col_sparse, double &r, double &f_cur,
-                                          double &sum_abs_b, uint32_t &perm_valid)
+// Weighted median, skip test, v_new and strict accept of one coordinate step
+// (ccd.py:81-91, :172-191), given this lane's breakpoint (loc, w).  CNTC > 0:
+// compile-time breakpoint count (dense column in a compile-time-n kernel),
+// so the reduction trees, tail lengths and bounds are constants.
+template <int PMAX, int CNTC>
+__device__ __forceinline__ void median_update(WarpShared<PMAX> *W, int lane, uint32_t inv_mask, int j, double lam,
+                                              bool cacheable, int cnt_rt, double loc, double w, double zsum,
+                                              bool have_zero, bool row, double xij, double bj, double &r,
+                                              double &f_cur, double &sum_abs_b, uint32_t &perm_valid)
 {
-    const double INF = __longlong_as_double(0x7ff0000000000000LL);
-    const int n = NC > 0 ? NC : n_rt;
-    const bool row = lane < n;
-    const double xij = xrow[j];  // lanes >= n read a stale in-bounds slot, never used
-    const double bj = W->B[j];
-    double loc, w, zsum = 0.0;
-    int cnt;
-    if (!col_sparse) {
-        const double q = ddiv(row ? r : 0.0, row ? xij : 1.0);  // np.divide then += b[j] (ccd.py:165-166)
-        loc = row ? dadd(q, bj) : (lane == n ? 0.0 : INF);
-        w = row ? fabs(xij) : (lane == n ? lam : 0.0);
-        cnt = n + 1;
-    } else {
-        sparse_column<PMAX>(W, lane, n, r, xij, bj, lam, loc, w, cnt, zsum);
-    }
-    // ---- weighted median (ccd.py:81-91): stable order by (location, index).
-    // The order is unique, so if this axis' permutation from the previous
-    // sweep is still sorted under the new locations it is the answer; the
-    // 15-stage network runs only when the check fails.
+    const int cnt = CNTC > 0 ? CNTC : cnt_rt;
+    // stable order by (location, index).  The order is unique, so if this
+    // axis' permutation from its previous evaluation is still sorted under the
+    // new locations it is the answer; otherwise odd-even transposition rounds
+    // repair a nearly sorted permutation, and the 15-stage network runs last.
     double key;
     int idx;
     bool sorted = false;
-    if (!col_sparse && ((perm_valid >> j) & 1u)) {
+    if (cacheable && ((perm_valid >> j) & 1u)) {
         idx = W->perm[j][lane];
         key = shfl_d(loc, idx);
         sorted = warp_is_sorted(key, idx, lane);
-        // nearly sorted (typical between sweeps): odd-even transposition rounds
 #pragma unroll 1
         for (int round = 0; round < 2 && !sorted; ++round) {
             oddeven_phase(key, idx, lane, 0);
@@ -343,9 +331,9 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_
         key = loc;
         idx = lane;
         bitonic32m(key, idx, inv_mask);
-        if (!col_sparse) W->perm[j][lane] = idx;
+        if (cacheable) W->perm[j][lane] = idx;
     }
-    perm_valid |= 1u << j;
+    if (cacheable) perm_valid |= 1u << j;
     const double ws = shfl_d(w, idx);
     double c = ws;
 #pragma unroll
@@ -353,17 +341,17 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_
         const double t = __shfl_up_sync(FULLMASK, c, d);
         if (lane >= d) c = dadd(c, t);
     }
-    const bool in = lane < cnt;
+    // pads carry weight 0, so their cumulative weight equals the total (>= half)
     double total = shfl_d(c, cnt - 1);
     double half = dmul(0.5, total);
-    int k = __popc(__ballot_sync(FULLMASK, in && c < half));
+    int k = __popc(__ballot_sync(FULLMASK, c < half));
     double ck = shfl_d(c, k < cnt ? k : cnt - 1);
     {
         // the parallel scan rounds differently from numpy's sequential cumsum
         // by at most ~6e-15 * total; every decision below is taken with a
         // 1e-13 * total margin or recomputed exactly
         const double marg = dmul(1e-13, total);
-        const bool risky = __any_sync(FULLMASK, in && fabs(dsub(c, half)) <= marg) ||
+        const bool risky = __any_sync(FULLMASK, lane < cnt && fabs(dsub(c, half)) <= marg) ||
                            fabs(dsub(fabs(dsub(ck, half)), dmul(1e-12, total))) <= marg;
         if (risky) exact_cumsum_decision(ws, lane, cnt, k, ck, total, half);
     }
@@ -372,11 +360,11 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_
     const double tk = shfl_d(key, ks);
     const double tk1 = shfl_d(key, ks + 1 < 32 ? ks + 1 : 31);
     const double t_new = tie ? dmul(0.5, dadd(tk, tk1)) : tk;
-    // ---- skip / evaluate / accept (ccd.py:172-191)
-    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
+    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
     double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
-    if (col_sparse) constant = dadd(constant, zsum);
-    // v_new: |t - loc| @ weights through OpenBLAS ddot's tree (see warp_blas_ddot)
+    if (have_zero) constant = dadd(constant, zsum);
+    // v_new = constant + |t - loc| @ weights, OpenBLAS ddot's order (see warp_blas_ddot)
+    const bool in = lane < cnt;
     const double a = in ? fabs(dsub(t_new, loc)) : 0.0;
     const double wv = in ? w : 0.0;
     const int n1 = cnt & -16;
@@ -407,12 +395,39 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_
         __syncwarp();
     }
     const double v_new = dadd(constant, dot);
-    if (v_new < f_cur) {  // strict accept
+    if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
         const double delta = dsub(t_new, bj);
         r = row ? dsub(r, dmul(xij, delta)) : r;
         sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
         f_cur = v_new;
         W->B[j] = t_new;  // every lane stores the same value: no cross-lane hazard
+    }
+}
+
+// One exact coordinate step on axis j (ccd.py:160-193), all lanes in lock-step.
+// NC > 0: compile-time row count (config shapes); NC == 0: runtime n_rt.
+template <int PMAX, int NC>
+__device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_t inv_mask, const double *xrow,
+                                          int n_rt, int j, double lam, bool col_sparse, double &r, double &f_cur,
+                                          double &sum_abs_b, uint32_t &perm_valid)
+{
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const int n = NC > 0 ? NC : n_rt;
+    const bool row = lane < n;
+    const double xij = xrow[j];  // lanes >= n read a stale in-bounds slot, never used
+    const double bj = W->B[j];
+    if (!col_sparse) {
+        const double q = ddiv(row ? r : 0.0, row ? xij : 1.0);  // np.divide then += b[j] (ccd.py:165-166)
+        const double loc = row ? dadd(q, bj) : (lane == n ? 0.0 : INF);
+        const double w = row ? fabs(xij) : (lane == n ? lam : 0.0);
+        median_update<PMAX, (NC > 0 ? NC + 1 : 0)>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, 0.0, false, row,
+                                                   xij, bj, r, f_cur, sum_abs_b, perm_valid);
+    } else {
+        double loc, w, zsum;
+        int cnt;
+        sparse_column<PMAX>(W, lane, n, r, xij, bj, lam, loc, w, cnt, zsum);
+        median_update<PMAX, 0>(W, lane, inv_mask, j, lam, false, cnt, loc, w, zsum, true, row, xij, bj, r, f_cur,
+                               sum_abs_b, perm_valid);
     }
 }
 
