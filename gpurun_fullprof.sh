@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python scripts/prof_locus.py --B 4736 > gpurun_out/plain.log 2>&1 && \
+timeout 1500 ncu --set full --import-source on --clock-control none -k regex:locus -c 1 -o gpurun_out/prof_cur python scripts/prof_locus.py --B 4736 > gpurun_out/ncu.log 2>&1; echo "full rc=$?"; cat gpurun_out/plain.log

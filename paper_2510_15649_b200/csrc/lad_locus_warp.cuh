@@ -417,7 +417,9 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX> *W, int lane, uint32_
     const double xij = xrow[j];  // lanes >= n read a stale in-bounds slot, never used
     const double bj = W->B[j];
     if (!col_sparse) {
-        const double q = ddiv(row ? r : 0.0, row ? xij : 1.0);  // np.divide then += b[j] (ccd.py:165-166)
+        // np.divide then += b[j] (ccd.py:165-166).  Pad lanes divide 1/1: a zero
+        // numerator would send the whole warp through __ddiv_rn's slow path.
+        const double q = ddiv(row ? r : 1.0, row ? xij : 1.0);
         const double loc = row ? dadd(q, bj) : (lane == n ? 0.0 : INF);
         const double w = row ? fabs(xij) : (lane == n ? lam : 0.0);
         median_update<PMAX, (NC > 0 ? NC + 1 : 0)>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, 0.0, false, row,
@@ -447,10 +449,11 @@ __device__ __forceinline__ double warp_objective(WarpShared<PMAX> *W, int lane, 
 // ccd_descend (ccd.py:126-206) for the descent request in C, all lanes.
 template <int PMAX, int NC>
 __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
-                                          int p_rt, uint32_t &perm_valid)
+                                          int p_rt, uint32_t &perm_valid_io)
 {
     const int n = NC > 0 ? NC : n_rt;
     const int p = NC > 0 ? PMAX : p_rt;
+    uint32_t perm_valid = perm_valid_io;  // register copy for the step loop
     const int frozen = C.req_frozen;
     const double tol = C.req_tol;
     const int max_sweeps = C.req_sweeps;
@@ -494,6 +497,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int
             j = j0;
         }
     }
+    perm_valid_io = perm_valid;
     __syncwarp();
     const double obj = warp_objective<PMAX>(W, lane, n, p, lam);
     const int D = C.D;
