@@ -335,27 +335,32 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX> *W, int lane, uin
     }
     if (cacheable) perm_valid |= 1u << j;
     const double ws = shfl_d(w, idx);
-    double c = ws;
+    // Cumulative weights only *locate* k = first cum >= total/2.  An FP32
+    // Kogge-Stone scan differs from numpy's sequential FP64 cumsum by at most
+    // ~6 * 2^-24 * total (conversion + 5 tree levels); every comparison with
+    // total/2 is accepted only beyond a 1e-5 * total margin, which also rules
+    // out the 1e-12 * total flat-segment tie.  Otherwise (or on FP32
+    // overflow/underflow) the exact FP64 sequential cumsum decides.
+    float cf = __double2float_rn(ws);
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const double t = __shfl_up_sync(FULLMASK, c, d);
-        if (lane >= d) c = dadd(c, t);
+        const float t = __shfl_up_sync(FULLMASK, cf, d);
+        if (lane >= d) cf = __fadd_rn(cf, t);
     }
     // pads carry weight 0, so their cumulative weight equals the total (>= half)
-    double total = shfl_d(c, cnt - 1);
-    double half = dmul(0.5, total);
-    int k = __popc(__ballot_sync(FULLMASK, c < half));
-    double ck = shfl_d(c, k < cnt ? k : cnt - 1);
-    {
-        // the parallel scan rounds differently from numpy's sequential cumsum
-        // by at most ~6e-15 * total; every decision below is taken with a
-        // 1e-13 * total margin or recomputed exactly
-        const double marg = dmul(1e-13, total);
-        const bool risky = __any_sync(FULLMASK, lane < cnt && fabs(dsub(c, half)) <= marg) ||
-                           fabs(dsub(fabs(dsub(ck, half)), dmul(1e-12, total))) <= marg;
-        if (risky) exact_cumsum_decision(ws, lane, cnt, k, ck, total, half);
+    const float totf = __shfl_sync(FULLMASK, cf, cnt - 1);
+    const float halff = 0.5f * totf;
+    int k = __popc(__ballot_sync(FULLMASK, cf < halff));
+    const float ckf = __shfl_sync(FULLMASK, cf, k < cnt ? k : cnt - 1);
+    const float margf = 1e-5f * totf;
+    const bool risky = !(totf > 0.0f && totf <= 3.0e38f) || fabsf(ckf - halff) <= margf ||
+                       __any_sync(FULLMASK, lane < cnt && fabsf(cf - halff) <= margf);
+    bool tie = false;
+    if (risky) {
+        double ck, total, half;
+        exact_cumsum_decision(ws, lane, cnt, k, ck, total, half);
+        tie = (k + 1 < cnt) && fabs(dsub(ck, half)) <= dmul(1e-12, total);
     }
-    const bool tie = (k + 1 < cnt) && fabs(dsub(ck, half)) <= dmul(1e-12, total);
     const int ks = k < cnt ? k : cnt - 1;
     const double tk = shfl_d(key, ks);
     const double tk1 = shfl_d(key, ks + 1 < 32 ? ks + 1 : 31);
