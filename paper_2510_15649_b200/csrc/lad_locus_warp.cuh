@@ -21,7 +21,7 @@
 namespace lad {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
-constexpr int WARPS_PER_BLOCK = 8;
+constexpr int WARPS_PER_BLOCK = 7;
 
 template <int PMAX>
 struct WarpShared {
@@ -522,7 +522,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX> *W, Ctl<PMAX> &C, int
 
 // PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
 template <int PMAX, int NC>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK) locus_warp_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4) locus_warp_kernel(LocusArgs A)
 {
     __shared__ WarpShared<PMAX> WS[WARPS_PER_BLOCK];
     const int lane = threadIdx.x & 31;
