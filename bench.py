@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=64, help="datasets (x16 lambdas) in the CPU baseline sample")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4],
+                    help="BASELINE config (2 = the metric's n=30/p=5 lambda path, the default)")
+    ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
     return ap.parse_args()
 
 
@@ -172,6 +175,74 @@ def run_reference(a, rank, world):
     print(json.dumps(line), flush=True)
 
 
+class Workload:
+    """One bench step's device inputs for a BASELINE config (inputs resident before timing)."""
+
+    def __init__(self, config, a, world, rank, dev):
+        import torch
+        from paper_2510_15649_b200 import generate as G
+        from paper_2510_15649_b200.distributed import block_for_step
+
+        self.config = config
+        self.variant = a.variant if config != 3 else "quadrature"
+        self.n, self.p = G.CONFIG_SHAPES[config]
+        self.dev = dev
+        self.data_index = None
+        self.steps_inputs = []
+        nsteps = a.warmup + a.steps
+        seed = SEED - 2 + config
+        if config == 2:
+            blk = a.block
+            self.desc = (f"config 2 lambda path: 2^20 datasets (n=30, p=5, config-0 distributions) x 16 lambdas "
+                         f"1e-2..1e1; step = {blk} datasets x 16 lambdas")
+            for s in range(nsteps):
+                first = block_for_step(s, world, rank, TOTAL_DATASETS // blk) * blk
+                X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
+                self.steps_inputs.append((X, Y))
+            self.data_index = torch.arange(blk, device=dev, dtype=torch.int64).repeat_interleave(16)
+            self.lam = torch.tensor(LAMBDA_GRID, device=dev, dtype=torch.float64).repeat(blk)
+            self.solves = blk * 16
+        elif config == 3:
+            X0, Y0 = G.config3_dataset(device=dev)
+            total = G.CONFIG_BATCH[3]
+            s0, e0 = [(total * r) // world for r in (rank, rank + 1)]
+            Xs, Ys = G.subsets(X0, Y0, 25, s0, e0 - s0)
+            self.desc = f"config 3: C(30,25)={total} row subsets of one dataset, lambda=0.5, quadrature"
+            self.steps_inputs = [(Xs, Ys)] * nsteps
+            self.lam = torch.full((e0 - s0,), 0.5, device=dev, dtype=torch.float64)
+            self.solves = e0 - s0
+        else:
+            B = {0: 256, 1: 1 << 20, 4: a.block4}[config]
+            self.desc = {0: "config 0: B=256, n=30, p=5, lambda=1, ternary",
+                         1: "config 1: B=2^20, n=10, p=2, lambda~U(0.1,2), thread-per-problem kernel",
+                         4: f"config 4: n=31, p=8, Student-t(3) X, Cauchy noise, lambda=1; step = {B} of the 2^26 problems"}[config]
+            lam_step = None
+            for s in range(nsteps):
+                first = (s * world + rank) * B
+                X, Y, L = G.generate(config, B, seed=seed, first=first, device=dev)
+                self.steps_inputs.append((X, Y, L))
+            self.lam = None
+            self.solves = B
+
+    def inputs(self, s):
+        t = self.steps_inputs[s]
+        if len(t) == 3:
+            return t[0], t[1], t[2]
+        return t[0], t[1], self.lam
+
+    def cpu_sample(self, s, max_solves):
+        """Exact bytes of the first problems of step s, expanded to (X, Y, lam) per solve."""
+        X, Y, L = self.inputs(s)
+        if self.data_index is not None:
+            nd = max(1, max_solves // 16)
+            Xh = np.repeat(X[:nd].cpu().numpy(), 16, axis=0)
+            Yh = np.repeat(Y[:nd].cpu().numpy(), 16, axis=0)
+            Lh = np.tile(LAMBDA_GRID, nd)
+            return Xh, Yh, Lh
+        m = min(max_solves, X.shape[0])
+        return X[:m].cpu().numpy(), Y[:m].cpu().numpy(), L[:m].cpu().numpy()
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -188,22 +259,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import paper_2510_15649_b200 as lad
-    from paper_2510_15649_b200 import generate as G
-    from paper_2510_15649_b200.distributed import block_for_step
     from paper_2510_15649_b200.solver import fp64_peak_tflops
 
-    blk = a.block
-    cfg = lad.LocusConfig(outer_search=a.variant)
-    nsteps = a.warmup + a.steps
-    # device-resident inputs for every step this rank will run (generated before timing)
-    blocks = []
-    for s in range(nsteps):
-        first = block_for_step(s, world, rank, TOTAL_DATASETS // blk) * blk
-        X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
-        blocks.append((first, X, Y))
-    data_index = torch.arange(blk, device=dev, dtype=torch.int64).repeat_interleave(16)
-    lam = torch.tensor(LAMBDA_GRID, device=dev, dtype=torch.float64).repeat(blk)
-    solves_per_step = blk * 16
+    wl = Workload(a.config, a, world, rank, dev)
+    cfg = lad.LocusConfig(outer_search=wl.variant)
+    solves_per_step = wl.solves
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     peak = fp64_peak_tflops()
@@ -213,8 +273,12 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def solve(s):
+        X, Y, L = wl.inputs(s)
+        return lad.solve_locus_batched(X, Y, L, cfg, data_index=wl.data_index)
+
     for s in range(a.warmup):
-        lad.solve_locus_batched(blocks[s][1], blocks[s][2], lam, cfg, data_index=data_index)
+        solve(s)
     barrier()
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
@@ -222,10 +286,9 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         for k in range(a.steps):
-            _, X, Y = blocks[a.warmup + k]
             flush.zero_()
             evs[k][0].record(stream)
-            r = lad.solve_locus_batched(X, Y, lam, cfg, data_index=data_index)
+            r = solve(a.warmup + k)
             evs[k][1].record(stream)
             results.append(r)
         barrier()
@@ -240,7 +303,7 @@ def main():
     # algorithmic flops of the timed launches (exact per-problem counters)
     S = sum(float(r.steps.double().sum()) for r in results)
     D = sum(float(r.descents.double().sum()) for r in results)
-    fl = flops_per_solve(S, D)
+    fl = flops_per_solve(S, D, wl.n, wl.p)
     achieved_tflops = fl / elapsed / 1e12
     status_ok = all(bool((r.status == 0).all()) for r in results)
     conv_frac = float(np.mean([float(r.converged.float().mean()) for r in results]))
@@ -249,59 +312,67 @@ def main():
     e2e_steps = a.e2e_steps if a.e2e_steps is not None else min(a.steps, 3)
     host = []
     for k in range(e2e_steps):
-        _, X, Y = blocks[a.warmup + k]
+        X, Y, L = wl.inputs(a.warmup + k)
         hx = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
         hy = torch.empty(Y.shape, dtype=torch.float64, pin_memory=True)
+        hl = torch.empty(L.shape, dtype=torch.float64, pin_memory=True)
         hx.copy_(X)
         hy.copy_(Y)
-        host.append((hx.numpy(), hy.numpy()))
-    hidx = torch.empty(data_index.shape, dtype=torch.int64, pin_memory=True)
-    hidx.copy_(data_index)
-    hlam = torch.empty(lam.shape, dtype=torch.float64, pin_memory=True)
-    hlam.copy_(lam)
-    hidx_np, hlam_np = hidx.numpy(), hlam.numpy()
+        hl.copy_(L)
+        host.append((hx.numpy(), hy.numpy(), hl.numpy()))
+    hidx_np = None
+    if wl.data_index is not None:
+        hidx = torch.empty(wl.data_index.shape, dtype=torch.int64, pin_memory=True)
+        hidx.copy_(wl.data_index)
+        hidx_np = hidx.numpy()
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        r = lad.solve_locus_batched(host[k][0], host[k][1], hlam_np, cfg, data_index=hidx_np)
+        r = lad.solve_locus_batched(host[k][0], host[k][1], host[k][2], cfg, data_index=hidx_np)
     barrier()
     e2e_elapsed = time.perf_counter() - t0
     te = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_steps * solves_per_step / float(te.item())
-    h2d = host[0][0].nbytes + host[0][1].nbytes + hlam_np.nbytes + hidx_np.nbytes
-    d2h = solves_per_step * (N_FEAT * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
+    h2d = host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes + (hidx_np.nbytes if hidx_np is not None else 0)
+    d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
 
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        first, X, Y = blocks[a.warmup]
-        ns = min(a.cpu_sample, blk)
-        Xh, Yh = X[:ns].cpu().numpy(), Y[:ns].cpu().numpy()
-        ro, dt, nth, nsol = run_cpu_sample(Xh, Yh, ns, a.variant)
+        Xh, Yh, Lh = wl.cpu_sample(a.warmup, a.cpu_sample * 16)
+        from oracle import oracle as O
+
+        O.build()
+        nth = cpu_threads()
+        t0 = time.perf_counter()
+        ro = O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=wl.variant)
+        dt = time.perf_counter() - t0
+        nsol = Xh.shape[0]
         cpu = {"value": nsol / dt, "unit": "solves/s", "cores": nth, "kind": "port",
-               "sample": f"{ns} config-2 datasets x 16 lambdas ({nsol} solves) of the first timed step, "
-                         f"CPU oracle (C restatement of solve_locus) on {nth} threads, {dt:.1f} s"}
+               "sample": f"first {nsol} solves of the first timed step, CPU oracle (C restatement of "
+                         f"solve_locus) on {nth} threads, {dt:.1f} s"}
         g = results[0]
-        gb = g.beta[: nsol].cpu().numpy()
-        go = g.objective[: nsol].cpu().numpy()
-        gs = g.steps[: nsol].cpu().numpy()
+        gb = g.beta[:nsol].cpu().numpy()
+        go = g.objective[:nsol].cpu().numpy()
+        gs = g.steps[:nsol].cpu().numpy()
         exact = int(np.sum(np.all(gb == ro["beta"], axis=1) & (go == ro["objective"]) & (gs == ro["steps"])))
         rel = np.abs(go - ro["objective"]) / np.abs(ro["objective"])
         parity = {"sample": nsol, "bit_exact": exact, "obj_within_1e-9": int(np.sum(rel <= 1e-9))}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
+            "metric": METRIC if a.config == 2 else f"LAD-LASSO solves/sec (config {a.config}, n={wl.n},p={wl.p} fp64)",
+            "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": elapsed_max * 1e3 / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device Philox generator, BASELINE config 2 distributions: X~N(0,1), "
-                    "2 nonzeros +-U[1,3], Laplace(0,0.5), 10% rows +-10)",
-            "config": {"workload": "config2_lambda_path", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
-                       "datasets_per_step_per_gpu": blk, "solves_per_step_per_gpu": solves_per_step,
-                       "variant": a.variant, "parallelism": f"shard{world} (independent problems, no collective)",
-                       "kernel": "warp-per-problem sm_100a", "l2": "flushed between steps (256 MiB memset)"},
+            "scaling": "weak" if a.config != 3 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox generator with the BASELINE config distributions)",
+            "config": {"workload": f"config{a.config}", "description": wl.desc, "n": wl.n, "p": wl.p,
+                       "solves_per_step_per_gpu": solves_per_step, "variant": wl.variant,
+                       "parallelism": f"shard{world} (independent problems, no collective)",
+                       "kernel": "thread-per-problem sm_100a" if a.config == 1 else "warp-per-problem sm_100a",
+                       "l2": "flushed between steps (256 MiB memset)"},
             "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_tflops / peak if peak else None, "traffic": None,
                          "peak_source": "measured DFMA loop on this GPU (lad_fp64_peak_tflops); "
