@@ -75,6 +75,10 @@ int lad_version(void);
 const char *lad_last_error(void);
 /* process-wide choice of the locus kernel mapping (both are bit-identical) */
 int lad_set_kernel_policy(int32_t policy);
+/* small batches (fewer problems than resident warps): run the independent
+ * per-axis searches of each problem as separate work items, then combine them
+ * in influence order (bit-identical; default on) */
+int lad_set_axis_parallel(int32_t enable);
 /* fills the defaults of LocusConfig()/CcdConfig() */
 void lad_default_params(lad_locus_params *prm);
 

@@ -16,6 +16,7 @@ SYMBOLS = (
     "lad_last_error",
     "lad_default_params",
     "lad_set_kernel_policy",
+    "lad_set_axis_parallel",
     "lad_locus_solve_f64",
     "lad_locus_solve_host_f64",
     "lad_ccd_descend_f64",
@@ -42,6 +43,11 @@ def set_kernel_policy(policy: int) -> None:
     rc = load().lad_set_kernel_policy(policy)
     if rc != LAD_OK:
         raise ValueError(last_error())
+
+
+def set_axis_parallel(enable: bool) -> None:
+    """Small-batch axis-parallel mode of the warp kernel (bit-identical results)."""
+    load().lad_set_axis_parallel(1 if enable else 0)
 
 
 class LocusParams(C.Structure):
@@ -99,6 +105,7 @@ def load(build_if_missing: bool = False):
     L.lad_default_params.argtypes = [C.POINTER(LocusParams)]
     L.lad_default_params.restype = None
     L.lad_set_kernel_policy.argtypes = [i32]
+    L.lad_set_axis_parallel.argtypes = [i32]
     L.lad_locus_solve_f64.argtypes = [vp, vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
     L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams),
                                            C.POINTER(LocusOut), vp]

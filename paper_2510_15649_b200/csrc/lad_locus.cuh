@@ -70,6 +70,10 @@ struct LocusArgs {
     double *seen;           // per lane slot: seen_cap * (1 + PMAX) doubles
     int seen_cap;
     unsigned long long *counter;
+    // axis-parallel mode (AXIS_SEARCH: item = problem * p + axis rank)
+    int axis_mode;
+    double *axis_res;   // (B * p) entries of axis_stride doubles
+    int axis_stride;
 };
 
 template <int PMAX>
@@ -92,7 +96,13 @@ enum : int {
     PC_PR_BEGIN, PC_PR_AFTER_COLD, PC_PR_AFTER_WARM, PC_PR_AFTER_FAST_ONLY, PC_PR_REFINE_CHECK,
     PC_PR_AFTER_REFINE, PC_PR_FINISH,
     PC_DESC_AFTER,
+    PC_FINISH_AXES,
 };
+
+// axis-parallel mode for small batches: the per-axis searches of solve_locus
+// share no state (locus.py:223-225), so they run as independent work items;
+// a finish pass replays them through the agreement rule in order.
+enum : int { AXIS_SERIAL = 0, AXIS_SEARCH = 1, AXIS_FINISH = 2 };
 
 enum : int { ACT_DESCENT = 0, ACT_EXIT = 1 };
 
@@ -100,6 +110,7 @@ template <int PMAX>
 struct Ctl {
     // problem
     int64_t prob;
+    int arank;  // axis rank of an AXIS_SEARCH item
     double lam;
     uint32_t sparse_mask;
     int pc, ret_pc;
@@ -286,9 +297,12 @@ struct ThreadAccess {
     __device__ __forceinline__ void sync() const {}
     __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
-        unsigned long long pr = atomicAdd(A.counter, 1ULL);
-        if ((int64_t)pr >= A.B) return -1;
+        const int div = A.axis_mode == AXIS_SEARCH ? p : 1;
+        unsigned long long item = atomicAdd(A.counter, 1ULL);
+        if ((int64_t)item >= A.B * div) return -1;
+        const unsigned long long pr = item / div;
         C.prob = (int64_t)pr;
+        C.arank = (int)(item % div);
         int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
         const double *xg = A.X + (size_t)src * n * p;
         const double *yg = A.Y + (size_t)src * n;
@@ -396,7 +410,31 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             C.nvals = C.rounds = C.calls = C.failures = 0;
             C.outer_ok = 1;
             C.confirmations = 0;
-            C.pc = PC_AXIS_START;
+            if (A.axis_mode == AXIS_SEARCH) {  // this item is one axis search of the problem
+                if (C.arank >= C.naxes) continue;
+                C.a_idx = C.arank;
+                C.pc = PC_AXIS_START;
+            } else {
+                C.pc = A.axis_mode == AXIS_FINISH ? PC_FINISH_AXES : PC_AXIS_START;
+            }
+            break;
+        }
+        // axis-parallel finish: replay the stored per-axis results in influence
+        // order through the same agreement rule (locus.py:338-362)
+        case PC_FINISH_AXES: {
+            const double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
+            C.axis = C.axes[C.a_idx];
+            C.ev_best.t = res[0];
+            for (int j = 0; j < p; ++j) C.ev_best.beta[j] = res[1 + j];
+            C.ev_best.value = res[1 + PMAX];
+            C.ev_best.conv = (int)res[2 + PMAX];
+            C.orounds = (int)res[3 + PMAX];
+            C.ev_calls = (int)res[4 + PMAX];
+            C.ev_failures = (int)res[5 + PMAX];
+            C.oconv = (int)res[6 + PMAX];
+            C.D += (int)res[7 + PMAX];
+            C.S += (long long)res[8 + PMAX];
+            C.pc = PC_AXIS_DONE;
             break;
         }
         case PC_DESC_AFTER: {
@@ -520,6 +558,23 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
         }
         // axis agreement bookkeeping (locus.py:338-362)
         case PC_AXIS_DONE: {
+            if (A.axis_mode == AXIS_SEARCH) {  // store this axis' result; the finish pass combines them
+                if (acc.leader()) {
+                    double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
+                    res[0] = C.ev_best.t;
+                    for (int j = 0; j < p; ++j) res[1 + j] = C.ev_best.beta[j];
+                    res[1 + PMAX] = C.ev_best.value;
+                    res[2 + PMAX] = C.ev_best.conv;
+                    res[3 + PMAX] = C.orounds;
+                    res[4 + PMAX] = C.ev_calls;
+                    res[5 + PMAX] = C.ev_failures;
+                    res[6 + PMAX] = C.oconv;
+                    res[7 + PMAX] = C.D;
+                    res[8 + PMAX] = (double)C.S;
+                }
+                C.pc = PC_FETCH;
+                break;
+            }
             Point<PMAX> &ab = C.ev_best;
             C.axis_values[C.nvals++] = ab.value;
             C.rounds += C.orounds;
@@ -541,7 +596,8 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             }
             if (p > 3 && C.confirmations >= 2) brk = true;
             C.a_idx++;
-            C.pc = (brk || C.a_idx >= C.naxes) ? PC_REFINE_START : PC_AXIS_START;
+            C.pc = (brk || C.a_idx >= C.naxes) ? PC_REFINE_START
+                                                : (A.axis_mode == AXIS_FINISH ? PC_FINISH_AXES : PC_AXIS_START);
             break;
         }
         // dense refinement plan (locus.py:363-395)

@@ -116,10 +116,12 @@ struct WarpAccess {
     __device__ __forceinline__ void sync() const { __syncwarp(); }
     __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
-        unsigned long long pr = 0;
-        if (lane == 0) pr = atomicAdd(A.counter, 1ULL);
-        pr = __shfl_sync(FULLMASK, pr, 0);
-        if ((int64_t)pr >= A.B) return -1;
+        const int div = A.axis_mode == AXIS_SEARCH ? p : 1;
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(A.counter, 1ULL);
+        item = __shfl_sync(FULLMASK, item, 0);
+        if ((int64_t)item >= A.B * div) return -1;
+        const unsigned long long pr = item / div;
         int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
         const double *xg = A.X + (size_t)src * n * p;
         const double *yg = A.Y + (size_t)src * n;
@@ -142,6 +144,7 @@ struct WarpAccess {
         ok = ok && isfinite(lraw) && lraw >= 0.0;
         __syncwarp();
         C.prob = (int64_t)pr;
+        C.arank = (int)(item % div);
         C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
         C.sparse_mask = mask;
         __syncwarp();
@@ -234,6 +237,15 @@ __device__ __forceinline__ bool warp_is_sorted(double key, int idx, int lane)
     return __all_sync(FULLMASK, ok);
 }
 
+// number of adjacent (key, idx) pairs out of ascending order
+__device__ __forceinline__ int warp_order_violations(double key, int idx, int lane)
+{
+    const double nk = shfl_down_d(key, 1);
+    const int ni = __shfl_down_sync(FULLMASK, idx, 1);
+    const bool ok = (lane == 31) || (key < nk) || ((key == nk) && (idx < ni));
+    return __popc(__ballot_sync(FULLMASK, !ok));
+}
+
 // One odd-even transposition phase: pairs (2i, 2i+1) for phase 0, (2i+1, 2i+2)
 // for phase 1; the lower lane of a pair keeps the smaller (key, idx).
 __device__ __forceinline__ void oddeven_phase(double &key, int &idx, int lane, int phase)
@@ -318,9 +330,11 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX> *W, int lane, uin
     if (cacheable && ((perm_valid >> j) & 1u)) {
         idx = W->perm[j][lane];
         key = shfl_d(loc, idx);
-        sorted = warp_is_sorted(key, idx, lane);
+        const int violations = warp_order_violations(key, idx, lane);
+        sorted = violations == 0;
+        // a few adjacent inversions: odd-even rounds; many: straight to the network
 #pragma unroll 1
-        for (int round = 0; round < 2 && !sorted; ++round) {
+        for (int round = 0; round < 2 && !sorted && violations <= 6; ++round) {
             oddeven_phase(key, idx, lane, 0);
             oddeven_phase(key, idx, lane, 1);
             sorted = warp_is_sorted(key, idx, lane);

@@ -84,6 +84,7 @@ Variant make_warp_variant()
 }
 
 int g_kernel_policy = LAD_KERNEL_AUTO;
+int g_axis_parallel = 1;
 
 bool pick_variant(int n, int p, Variant &v)
 {
@@ -152,8 +153,14 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.block, v.smem));
     if (per_sm < 1) return fail(LAD_E_CUDA, "locus kernel does not fit on an SM (smem %zu)", v.smem);
-    int64_t want = (B + v.slots_per_block - 1) / v.slots_per_block;
-    int64_t grid = std::min<int64_t>(want, (int64_t)g_num_sms * per_sm);
+    const int64_t max_grid = (int64_t)g_num_sms * per_sm;
+    // Small batches leave most warps idle and are bound by one solve's latency:
+    // run the independent per-axis searches as separate work items (warp kernel).
+    const bool axis_par = g_axis_parallel && mode == lad::MODE_LOCUS && v.block > 32 && prm->outer_axis < 0 &&
+                          p > 1 && B < max_grid * v.slots_per_block;
+    const int64_t items = axis_par ? B * p : B;
+    int64_t want = (items + v.slots_per_block - 1) / v.slots_per_block;
+    int64_t grid = std::min<int64_t>(want, max_grid);
     int64_t slots = grid * v.slots_per_block;
 
     lad::LocusArgs A;
@@ -181,20 +188,44 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
     A.steps = out->steps;
     A.seen_cap = mode == lad::MODE_LOCUS ? seen_capacity(prm, p) : 0;
     size_t seen_bytes = (size_t)slots * A.seen_cap * (1 + v.pmax) * sizeof(double);
-    size_t scratch = seen_bytes + 256;
+    A.axis_stride = v.pmax + 10;
+    size_t axis_bytes = axis_par ? (size_t)B * p * A.axis_stride * sizeof(double) : 0;
+    size_t scratch = 256 + seen_bytes + axis_bytes;
     char *buf = nullptr;
     CK(cudaMallocAsync((void **)&buf, scratch, st));
     A.counter = (unsigned long long *)buf;
     A.seen = A.seen_cap ? (double *)(buf + 256) : nullptr;
+    A.axis_res = axis_par ? (double *)(buf + 256 + seen_bytes) : nullptr;
     CK(cudaMemsetAsync(buf, 0, 256, st));
-    v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
-    cudaError_t le = cudaGetLastError();
+    cudaError_t le;
+    if (!axis_par) {
+        A.axis_mode = lad::AXIS_SERIAL;
+        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
+        le = cudaGetLastError();
+    } else {
+        A.axis_mode = lad::AXIS_SEARCH;
+        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
+        le = cudaGetLastError();
+        A.axis_mode = lad::AXIS_FINISH;
+        A.counter = (unsigned long long *)(buf + 64);
+        int64_t grid2 = std::min<int64_t>((B + v.slots_per_block - 1) / v.slots_per_block, max_grid);
+        if (le == cudaSuccess) {
+            v.fn<<<(unsigned)grid2, v.block, v.smem, st>>>(A);
+            le = cudaGetLastError();
+        }
+    }
     cudaFreeAsync(buf, st);
     if (le != cudaSuccess) return fail(LAD_E_CUDA, "locus kernel launch: %s", cudaGetErrorString(le));
     return LAD_OK;
 }
 
 }  // namespace
+
+extern "C" int lad_set_axis_parallel(int32_t enable)
+{
+    g_axis_parallel = enable != 0;
+    return LAD_OK;
+}
 
 extern "C" int lad_set_kernel_policy(int32_t policy)
 {

@@ -324,6 +324,26 @@ def test_config0_full_batch_against_oracle(oracle):
         _oracle_sample_exact(oracle, X, Y, L, r, np.arange(256), v)
 
 
+@pytest.mark.parametrize("axis_parallel", [False, True])
+def test_axis_parallel_small_batch_mode_bit_exact(axis_parallel):
+    """Small batches may split each solve into independent per-axis work items
+    (locus.py:223-225) recombined in order; both modes must equal the reference."""
+    from paper_2510_15649_b200 import _lib
+
+    _lib.set_axis_parallel(axis_parallel)
+    try:
+        for name, v in (("cfg0", "ternary"), ("cfg0", "quadrature"), ("cfg4", "ternary"), ("cfg2", "ternary")):
+            g = load_golden(name)
+            r = lad.solve_locus_batched(g["x"], g["y"], g["lam"], lad.LocusConfig(outer_search=v))
+            rr = dict(beta=r.beta, objective=r.objective, iterations=r.iterations, objective_evals=r.objective_evals,
+                      converged=r.converged, D=r.descents, S=r.steps)
+            _assert_exact(rr, g, v)
+        g = load_golden("acceptance")
+        _assert_exact(_locus_groups(g, "ternary"), g, "ternary")
+    finally:
+        _lib.set_axis_parallel(True)
+
+
 def test_generator_shards_are_reproducible():
     """Problem i depends only on (seed, i): shards generated separately equal one big generation."""
     for config in (0, 1, 2, 4):
