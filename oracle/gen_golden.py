@@ -382,6 +382,78 @@ def gen_configs(pool, quick=False):
     _locus_fixture(pool, "cfg4", X, Y, 1.0, ("ternary",), extra=dict(beta_true=bt))
 
 
+def _run_ref_cli(argv):
+    """Run the reference CLI in-process; return (exit code, stdout, stderr)."""
+    import contextlib
+    import io
+
+    _ref()
+    from ladlasso import cli
+
+    out, err = io.StringIO(), io.StringIO()
+    with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+        code = cli.main(argv)
+    return code, out.getvalue(), err.getvalue()
+
+
+def gen_cli(pool):
+    """Reference CLI transcripts (cli.py) for tests/test_cli.py: gen files, solve RESULT
+    lines, check/bench CSVs.  Wall-time fields are kept verbatim; the tests drop them."""
+    import json
+    import tempfile
+
+    _ref()
+    from ladlasso.rng import Pcg32
+
+    fx = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        # gen: CSV + sidecar bytes for a few specs
+        fx["gen"] = []
+        for spec in (["--m", "7", "--d", "3", "--seed", "11"],
+                     ["--m", "12", "--d", "2", "--n-informative", "1", "--noise-sigma", "0.5",
+                      "--outlier-fraction", "0.25", "--outlier-scale", "20", "--seed", "3"],
+                     ["--m", "30", "--d", "5", "--outlier-fraction", "0.1", "--seed", "123456789"]):
+            path = os.path.join(tmp, "g.csv")
+            code, so, _ = _run_ref_cli(["gen", path] + spec)
+            with open(path) as fh, open(path + ".meta.json") as fm:
+                fx["gen"].append(dict(argv=spec, code=code, stdout=so, csv=fh.read(), meta=fm.read()))
+        # solve: every in-scope solver on one generated dataset
+        path = os.path.join(tmp, "s.csv")
+        _run_ref_cli(["gen", path, "--m", "11", "--d", "3", "--outlier-fraction", "0.2", "--seed", "77"])
+        with open(path) as fh:
+            fx["solve_csv"] = fh.read()
+        fx["solve"] = []
+        for solver in ("locus_ternary", "locus_quadrature", "brute", "ccd_plain"):
+            for lam in ("0.05", "1.5"):
+                argv = ["solve", path, "--lambda", lam, "--solver", solver]
+                code, so, _ = _run_ref_cli(argv)
+                fx["solve"].append(dict(argv=argv[2:], code=code, stdout=so))
+        # check: per-instance CSV of a small seeded sweep
+        fx["check"] = []
+        for argv in (["--n-instances", "16", "--seed", "5"],
+                     ["--n-instances", "12", "--seed", "2", "--d", "1-2", "--m", "5,8", "--lambda", "0.3,2"]):
+            out = os.path.join(tmp, "c.csv")
+            code, so, _ = _run_ref_cli(["check"] + argv + ["--out", out])
+            with open(out) as fh:
+                fx["check"].append(dict(argv=argv, code=code, stdout=so, csv=fh.read()))
+        # check task picker for the default 50-instance sweep (d, m, lambda, seed)
+        picker = Pcg32(0)
+        d_set, m_set, l_set = [1, 2, 3], list(range(4, 13)), [0.01, 0.1, 1.0]
+        fx["check_tasks_seed0"] = [[d_set[picker.below(3)], m_set[picker.below(9)], l_set[picker.below(3)],
+                                    0 + 1_000_003 * (i + 1)] for i in range(50)]
+        # bench: runs + medians CSVs (no lp)
+        out = os.path.join(tmp, "b.csv")
+        argv = ["--d", "1,2,3", "--m", "6,10", "--repeats", "2", "--seed", "4",
+                "--solvers", "brute,locus_ternary,locus_quadrature,ccd_plain"]
+        code, so, _ = _run_ref_cli(["bench"] + argv + ["--out", out])
+        with open(out) as fh, open(os.path.join(tmp, "b_medians.csv")) as fm:
+            fx["bench"] = dict(argv=argv, code=code, csv=fh.read(), medians=fm.read())
+    with open(os.path.join(GOLDEN, "cli.json"), "w") as fh:
+        json.dump(fx, fh, indent=1)
+        fh.write("\n")
+    print("wrote cli.json")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count())
@@ -392,7 +464,8 @@ def main():
     only = set(a.only.split(",")) if a.only else None
     with Pool(a.procs) as pool:
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
-                         ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick))):
+                         ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
+                         ("cli", gen_cli)):
             if only is None or name in only:
                 fn(pool)
 

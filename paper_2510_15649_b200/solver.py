@@ -272,7 +272,7 @@ def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
         Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
-        bt = torch.from_numpy(np.ascontiguousarray(beta, dtype=np.float64)).to(dev)
+        bt = torch.from_numpy(np.array(beta, dtype=np.float64, order="C")).to(dev)
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
