@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4],
                     help="BASELINE config (2 = the metric's n=30/p=5 lambda path, the default)")
     ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
+                    help="f32: the fp32 mode (binary32 data and descents; config 4 runs in both)")
     return ap.parse_args()
 
 
@@ -179,6 +181,13 @@ class Workload:
     """One bench step's device inputs for a BASELINE config (inputs resident before timing)."""
 
     def __init__(self, config, a, world, rank, dev):
+        self._build(config, a, world, rank, dev)
+        if a.dtype == "f32":  # generated in binary64, rounded once to binary32 on the device
+            self.steps_inputs = [tuple(t.float() for t in inp) for inp in self.steps_inputs]
+            if self.lam is not None:
+                self.lam = self.lam.float()
+
+    def _build(self, config, a, world, rank, dev):
         import torch
         from paper_2510_15649_b200 import generate as G
         from paper_2510_15649_b200.distributed import block_for_step
@@ -259,14 +268,16 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import paper_2510_15649_b200 as lad
-    from paper_2510_15649_b200.solver import fp64_peak_tflops
+    from paper_2510_15649_b200 import _lib
+    from paper_2510_15649_b200.solver import fp32_peak_tflops, fp64_peak_tflops
 
     wl = Workload(a.config, a, world, rank, dev)
     cfg = lad.LocusConfig(outer_search=wl.variant)
     solves_per_step = wl.solves
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
-    peak = fp64_peak_tflops()
+    peak = fp32_peak_tflops() if a.dtype == "f32" else fp64_peak_tflops()
+    hdt = torch.float32 if a.dtype == "f32" else torch.float64
 
     def barrier():
         if world > 1:
@@ -283,6 +294,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     results = []
+    launches0 = _lib.kernel_launches()
     with ClockSampler(local) as clk:
         barrier()
         for k in range(a.steps):
@@ -292,6 +304,7 @@ def main():
             evs[k][1].record(stream)
             results.append(r)
         barrier()
+    gpu_launches = _lib.kernel_launches() - launches0
     clocks = clk.summary()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     elapsed = sum(step_ms) / 1e3
@@ -313,9 +326,9 @@ def main():
     host = []
     for k in range(e2e_steps):
         X, Y, L = wl.inputs(a.warmup + k)
-        hx = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
-        hy = torch.empty(Y.shape, dtype=torch.float64, pin_memory=True)
-        hl = torch.empty(L.shape, dtype=torch.float64, pin_memory=True)
+        hx = torch.empty(X.shape, dtype=hdt, pin_memory=True)
+        hy = torch.empty(Y.shape, dtype=hdt, pin_memory=True)
+        hl = torch.empty(L.shape, dtype=hdt, pin_memory=True)
         hx.copy_(X)
         hy.copy_(Y)
         hl.copy_(L)
@@ -346,13 +359,15 @@ def main():
 
         O.build()
         nth = cpu_threads()
+        if a.dtype == "f32":
+            Xh, Yh, Lh = Xh.astype(np.float32), Yh.astype(np.float32), np.asarray(Lh, dtype=np.float32)
         t0 = time.perf_counter()
         ro = O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=wl.variant)
         dt = time.perf_counter() - t0
         nsol = Xh.shape[0]
         cpu = {"value": nsol / dt, "unit": "solves/s", "cores": nth, "kind": "port",
                "sample": f"first {nsol} solves of the first timed step, CPU oracle (C restatement of "
-                         f"solve_locus) on {nth} threads, {dt:.1f} s"}
+                         f"solve_locus{', binary32 build' if a.dtype == 'f32' else ''}) on {nth} threads, {dt:.1f} s"}
         g = results[0]
         gb = g.beta[:nsol].cpu().numpy()
         go = g.objective[:nsol].cpu().numpy()
@@ -363,27 +378,29 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC if a.config == 2 else f"LAD-LASSO solves/sec (config {a.config}, n={wl.n},p={wl.p} fp64)",
+            "metric": METRIC if (a.config == 2 and a.dtype == "f64") else
+            f"LAD-LASSO solves/sec (config {a.config}, n={wl.n},p={wl.p} {a.dtype.replace('f', 'fp')})",
             "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": elapsed_max * 1e3 / a.steps, "higher_is_better": True,
-            "scaling": "weak" if a.config != 3 else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if a.config != 3 else "strong", "vs_baseline": None, "dtype": a.dtype,
             "data": "synthetic (device Philox generator with the BASELINE config distributions)",
             "config": {"workload": f"config{a.config}", "description": wl.desc, "n": wl.n, "p": wl.p,
                        "solves_per_step_per_gpu": solves_per_step, "variant": wl.variant,
                        "parallelism": f"shard{world} (independent problems, no collective)",
                        "kernel": "thread-per-problem sm_100a" if a.config == 1 else "warp-per-problem sm_100a",
                        "l2": "flushed between steps (256 MiB memset)"},
-            "roofline": {"bound": "fp64", "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved_tflops / peak if peak else None, "traffic": None,
-                         "peak_source": "measured DFMA loop on this GPU (lad_fp64_peak_tflops); "
-                                        "MEASURED_PEAKS.json has no FP64 figure",
+            "roofline": {"bound": "fp64" if a.dtype == "f64" else "fp32", "achieved": achieved_tflops, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None, "traffic": None,
+                         "peak_source": (f"measured {'DFMA' if a.dtype == 'f64' else 'FFMA'} loop on this GPU "
+                                         f"(lad_{a.dtype.replace('f', 'fp')}_peak_tflops); "
+                                         "MEASURED_PEAKS.json has no FP64/FP32 CUDA-core figure"),
                          "flops_per_solve": fl / (a.steps * solves_per_step),
                          "coord_steps_per_solve": S / (a.steps * solves_per_step),
                          "descents_per_solve": D / (a.steps * solves_per_step)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
-            "gpu_launches": a.steps,
+            "gpu_launches": gpu_launches,
             "clocks": clocks,
             "status_ok": status_ok,
             "converged_frac": conv_frac,

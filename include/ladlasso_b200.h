@@ -8,6 +8,8 @@
  *
  *   lad_locus_solve_f64     <- locus.solve_locus(spec, cfg)        locus.py:300-409
  *   lad_locus_solve_host_f64   same, host buffers (H2D + solve + D2H inside)
+ *   lad_locus_solve_f32 / _host_f32 / lad_ccd_descend_f32: the fp32 mode
+ *                              (BASELINE config 4 "fp64 and fp32"), see below
  *   lad_ccd_descend_f64     <- ccd.ccd_descend(spec, start, cfg)   ccd.py:126-206
  *   lad_brute_solve_f64     <- brute.solve_brute(spec, ...)        brute.py:106-145
  *   lad_objective_f64       <- model.evaluate_objective(spec, b)   model.py:151-154
@@ -73,6 +75,8 @@ typedef struct lad_locus_out {
 
 int lad_version(void);
 const char *lad_last_error(void);
+/* number of kernels this library has launched so far (process-wide) */
+long long lad_kernel_launches(void);
 /* process-wide choice of the locus kernel mapping (both are bit-identical) */
 int lad_set_kernel_policy(int32_t policy);
 /* small batches (fewer problems than resident warps): run the independent
@@ -107,9 +111,29 @@ int lad_brute_solve_f64(const double *X, const double *Y, const double *lam, int
                         int32_t max_variables, int64_t max_candidates, double lambda_floor, double *beta,
                         double *objective, int64_t *vertices, void *stream);
 
-/* Roofline denominator: measured dense FP64 FMA throughput of the current
- * device (TFLOP/s, 2 flops per DFMA), timed with CUDA events on `stream`. */
+/* fp32 mode.  The reference has no binary32 path (model.py:33 casts every
+ * input to float64), so this mode is defined by this library: X, Y, lambda are
+ * binary32 and every coordinate-descent operation (residuals, breakpoints, the
+ * weighted median, v_new, objectives) runs in binary32 in the same order as
+ * the fp64 path, while the outer search (brackets, probe positions, warm
+ * starts, agreement and refine rules) stays binary64; a probe position or
+ * warm start is rounded to binary32 when its descent starts.  Outputs are
+ * binary64 (exact widenings).  Parity: bit-exact against the oracle compiled
+ * for binary32 (oracle/orc_descent.inc); distance to the fp64 reference is a
+ * reported statistic, not a guarantee.  n <= 31, p <= 8 (warp kernel). */
+int lad_locus_solve_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index, int64_t B,
+                        int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+int lad_locus_solve_host_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,
+                             int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                             const lad_locus_out *out, void *stream);
+int lad_ccd_descend_f32(const float *X, const float *Y, const float *lam, int64_t B, int32_t n, int32_t p,
+                        const double *start, const int32_t *frozen, double sweep_tolerance, int32_t max_sweeps,
+                        double lambda_floor, const lad_locus_out *out, void *stream);
+
+/* Roofline denominators: measured dense FP64 / FP32 FMA throughput of the
+ * current device (TFLOP/s, 2 flops per FMA), timed with CUDA events on `stream`. */
 int lad_fp64_peak_tflops(double *tflops, void *stream);
+int lad_fp32_peak_tflops(double *tflops, void *stream);
 
 /* evaluate_objective for (B, p) coefficient vectors. */
 int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,

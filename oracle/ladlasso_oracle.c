@@ -52,136 +52,65 @@
 #define ORC_MAX_M 64
 
 /* ------------------------------------------------------------------ */
-/* numerics models                                                      */
+/* problem + coordinate descent (ccd.py:126-206)                        */
 /* ------------------------------------------------------------------ */
 
-/* numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src), n <= 128 */
-double orc_np_sum(const double *a, int n)
-{
-    if (n < 8) {
-        double res = 0.0;
-        for (int i = 0; i < n; ++i) res += a[i];
-        return res;
-    }
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    int lim = n - (n % 8);
-    for (; i < lim; i += 8)
-        for (int j = 0; j < 8; ++j) r[j] += a[i + j];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res += a[i];
-    return res;
-}
 
-static double np_sum_abs(const double *a, int n)
-{
-    double t[ORC_MAX_M + 1];
-    for (int i = 0; i < n; ++i) t[i] = fabs(a[i]);
-    return orc_np_sum(t, n);
-}
+typedef struct {
+    const double *x; /* (m, d) row-major */
+    const double *y; /* (m,) */
+    int m, d;
+    double lam;      /* lambda_eff = max(lam, floor) */
+    const float *xf, *yf; /* fp32 mode: the binary32 data (x, y unused) */
+    int f32;
+} orc_problem;
 
-/* OpenBLAS ddot_k, SkylakeX build, 0 <= n <= 47 (enough for n+1 <= 33 breakpoints) */
-double orc_ddot(const double *x, const double *y, int n)
-{
-    int n1 = n & -16;
-    double dot = 0.0;
-    if (n1 == 16) {
-        double p[16], S[4];
-        for (int i = 0; i < 16; ++i) p[i] = x[i] * y[i];
-        for (int l = 0; l < 4; ++l) S[l] = ((p[l] + p[l + 4]) + p[l + 8]) + p[l + 12];
-        dot = (S[0] + S[2]) + (S[1] + S[3]);
-    } else if (n1 == 32) {
-        double p[32], A[4][4], S[4];
-        for (int i = 0; i < 32; ++i) p[i] = x[i] * y[i];
-        for (int k = 0; k < 4; ++k)
-            for (int l = 0; l < 4; ++l) A[k][l] = p[8 * k + l] + p[8 * k + l + 4];
-        for (int l = 0; l < 4; ++l) S[l] = ((A[0][l] + A[1][l]) + A[2][l]) + A[3][l];
-        dot = (S[0] + S[2]) + (S[1] + S[3]);
-    } else if (n1 > 32) {
-        abort(); /* not modelled; never reached for n <= 47 */
-    }
-    for (int i = n1; i < n; ++i) dot = fma(x[i], y[i], dot);
-    return dot;
-}
+typedef struct {
+    double beta[ORC_MAX_D];
+    double objective;
+    int sweeps, steps, converged;
+} orc_descent;
 
-/* One output of x @ b via OpenBLAS dgemv_t (SkylakeX) for a C-order (m, d) x,
- * d <= 8.  `row` selects which kernel the row is computed by. */
-double orc_gemv_row(const double *xr, const double *b, int d, int row, int m)
-{
-    int nb = d & -4, m3 = d & 3;
-    double p[8];
-    double S = 0.0;
-    for (int j = 0; j < nb; ++j) p[j] = xr[j] * b[j];
-    if (nb == 4) {
-        S = (p[0] + p[2]) + (p[1] + p[3]);
-    } else if (nb == 8) {
-        int g4 = 4 * (m >> 2);
-        if (row < g4) {                      /* dgemv_kernel_4x4 */
-            double q[4];
-            for (int l = 0; l < 4; ++l) q[l] = fma(xr[l + 4], b[l + 4], p[l]);
-            S = (q[0] + q[2]) + (q[1] + q[3]);
-        } else if ((m & 2) && row < g4 + 2) {  /* dgemv_kernel_4x2 */
-            double L0 = ((p[0] + p[2]) + p[4]) + p[6];
-            double L1 = ((p[1] + p[3]) + p[5]) + p[7];
-            S = L0 + L1;
-        } else {                               /* dgemv_kernel_4x1 */
-            S = ((p[0] + p[4]) + (p[2] + p[6])) + ((p[1] + p[5]) + (p[3] + p[7]));
-        }
-    }
-    if (m3 == 1) {
-        S = fma(xr[nb], b[nb], S);
-    } else if (m3 == 2) {
-        S = S + fma(xr[nb], b[nb], xr[nb + 1] * b[nb + 1]);
-    } else if (m3 == 3) {
-        S = S + fma(xr[nb + 2], b[nb + 2], fma(xr[nb], b[nb], xr[nb + 1] * b[nb + 1]));
-    }
-    return S;
-}
+typedef struct {
+    long long descents;
+    long long steps;
+} orc_counters;
 
-/* residual r = y - x @ b  (model.py:147, ccd.py:148) */
-static void residual_init(const double *x, const double *y, int m, int d, const double *b, double *r)
-{
-    for (int i = 0; i < m; ++i) r[i] = y[i] - orc_gemv_row(x + (size_t)i * d, b, d, i, m);
-}
 
-/* model.objective_value (model.py:145-148) */
-double orc_objective(const double *x, const double *y, int m, int d, double lam, const double *b)
-{
-    double r[ORC_MAX_M];
-    residual_init(x, y, m, d, b, r);
-    return np_sum_abs(r, m) + lam * np_sum_abs(b, d);
-}
+/* the descent half, once per element type (orc_descent.inc) */
+#define REAL double
+#define RF(name) name
+#define R_FABS fabs
+#define R_FMA fma
+#define R_X(P) ((P)->x)
+#define R_Y(P) ((P)->y)
+#include "orc_descent.inc"
+#undef REAL
+#undef RF
+#undef R_FABS
+#undef R_FMA
+#undef R_X
+#undef R_Y
+#define REAL float
+#define RF(name) name##_f32
+#define R_FABS fabsf
+#define R_FMA fmaf
+#define R_X(P) ((P)->xf)
+#define R_Y(P) ((P)->yf)
+#include "orc_descent.inc"
+#undef REAL
+#undef RF
+#undef R_FABS
+#undef R_FMA
+#undef R_X
+#undef R_Y
 
-/* ------------------------------------------------------------------ */
-/* weighted median (ccd.py:81-91)                                       */
-/* ------------------------------------------------------------------ */
-
-double orc_median_location(const double *loc, const double *w, int n)
+/* precision dispatch: the outer search is binary64 in both modes */
+static void ccd_descend(const orc_problem *P, const double *start, int frozen, double sweep_tol, int max_sweeps,
+                        orc_descent *out, orc_counters *cnt, double *trace, int *trace_len)
 {
-    int order[ORC_MAX_M + 1];
-    /* stable argsort by location: insertion sort, ties keep index order */
-    for (int i = 0; i < n; ++i) {
-        int k = i;
-        while (k > 0 && loc[order[k - 1]] > loc[i]) {
-            order[k] = order[k - 1];
-            --k;
-        }
-        order[k] = i;
-    }
-    double cum[ORC_MAX_M + 1];
-    double c = 0.0;
-    for (int i = 0; i < n; ++i) {
-        c += w[order[i]];
-        cum[i] = c;
-    }
-    double total = cum[n - 1];
-    double half = 0.5 * total;
-    int k = 0;
-    while (k < n && cum[k] < half) ++k; /* searchsorted side='left' */
-    if (k + 1 < n && fabs(cum[k] - half) <= 1e-12 * total)
-        return 0.5 * (loc[order[k]] + loc[order[k + 1]]);
-    return loc[order[k < n - 1 ? k : n - 1]];
+    if (P->f32) descend_f32(P, start, frozen, sweep_tol, max_sweeps, out, cnt, trace, trace_len);
+    else descend(P, start, frozen, sweep_tol, max_sweeps, out, cnt, trace, trace_len);
 }
 
 /* linesearch.weighted_median_min (linesearch.py:133-154): total = weights.sum() */
@@ -217,114 +146,6 @@ double orc_weighted_median_min(const double *loc, const double *w, int n, double
     return t;
 }
 
-/* ------------------------------------------------------------------ */
-/* problem + coordinate descent (ccd.py:126-206)                        */
-/* ------------------------------------------------------------------ */
-
-typedef struct {
-    const double *x; /* (m, d) row-major */
-    const double *y; /* (m,) */
-    int m, d;
-    double lam;      /* lambda_eff = max(lam, floor) */
-} orc_problem;
-
-typedef struct {
-    double beta[ORC_MAX_D];
-    double objective;
-    int sweeps, steps, converged;
-} orc_descent;
-
-typedef struct {
-    long long descents;
-    long long steps;
-} orc_counters;
-
-static void ccd_descend(const orc_problem *P, const double *start, int frozen, double sweep_tol,
-                        int max_sweeps, orc_descent *out, orc_counters *cnt, double *trace, int *trace_len)
-{
-    const int m = P->m, d = P->d;
-    const double lam = P->lam;
-    double b[ORC_MAX_D];
-    double r[ORC_MAX_M];
-    memcpy(b, start, sizeof(double) * d);
-    residual_init(P->x, P->y, m, d, b, r);
-    double f_cur = np_sum_abs(r, m) + lam * np_sum_abs(b, d);
-
-    /* _AxisWorkspace per axis (ccd.py:94-110) */
-    int nz_idx[ORC_MAX_D][ORC_MAX_M], nnz[ORC_MAX_D], zero_idx[ORC_MAX_D][ORC_MAX_M], nzero[ORC_MAX_D];
-    double weights[ORC_MAX_D][ORC_MAX_M + 1];
-    for (int j = 0; j < d; ++j) {
-        nnz[j] = nzero[j] = 0;
-        for (int i = 0; i < m; ++i) {
-            double c = P->x[(size_t)i * d + j];
-            if (c != 0.0) nz_idx[j][nnz[j]++] = i;
-            else zero_idx[j][nzero[j]++] = i;
-        }
-        for (int k = 0; k < nnz[j]; ++k) weights[j][k] = fabs(P->x[(size_t)nz_idx[j][k] * d + j]);
-        weights[j][nnz[j]] = lam;
-    }
-    int evals = 0, sweeps = 0, converged = 0;
-    double locs[ORC_MAX_M + 1];
-    for (int s = 0; s < max_sweeps; ++s) {
-        ++sweeps;
-        double f_sweep_start = f_cur;
-        double sum_abs_b = np_sum_abs(b, d);
-        for (int j = 0; j < d; ++j) {
-            if (j == frozen) continue;
-            int k = nnz[j];
-            if (k == m) { /* dense: np.divide then += b[j] */
-                for (int i = 0; i < m; ++i) {
-                    locs[i] = r[i] / P->x[(size_t)i * d + j];
-                    locs[i] += b[j];
-                }
-            } else {      /* base = residual[nz] + col_nz * b[j]; base / col_nz */
-                for (int q = 0; q < k; ++q) {
-                    double c = P->x[(size_t)nz_idx[j][q] * d + j];
-                    double base = r[nz_idx[j][q]] + c * b[j];
-                    locs[q] = base / c;
-                }
-            }
-            locs[k] = 0.0;
-            double t_new = orc_median_location(locs, weights[j], k + 1);
-            ++evals;
-            if (fabs(t_new - b[j]) <= 1e-14 * (1.0 + fabs(b[j]))) {
-                if (trace) trace[(*trace_len)++] = f_cur;
-                continue;
-            }
-            double constant = lam * (sum_abs_b - fabs(b[j]));
-            if (nzero[j]) {
-                double zr[ORC_MAX_M];
-                for (int q = 0; q < nzero[j]; ++q) zr[q] = fabs(r[zero_idx[j][q]]);
-                constant += orc_np_sum(zr, nzero[j]);
-            }
-            double a[ORC_MAX_M + 1];
-            for (int q = 0; q <= k; ++q) a[q] = fabs(t_new - locs[q]);
-            double v_new = constant + orc_ddot(a, weights[j], k + 1);
-            if (v_new < f_cur) {
-                double delta = t_new - b[j];
-                for (int i = 0; i < m; ++i) r[i] -= P->x[(size_t)i * d + j] * delta;
-                sum_abs_b += fabs(t_new) - fabs(b[j]);
-                b[j] = t_new;
-                f_cur = v_new;
-            }
-            if (trace) trace[(*trace_len)++] = f_cur;
-        }
-        if (f_sweep_start - f_cur < sweep_tol) {
-            converged = 1;
-            break;
-        }
-    }
-    memcpy(out->beta, b, sizeof(double) * d);
-    out->objective = orc_objective(P->x, P->y, m, d, lam, b);
-    out->sweeps = sweeps;
-    out->steps = evals;
-    out->converged = converged;
-    if (cnt) {
-        cnt->descents += 1;
-        cnt->steps += evals;
-    }
-}
-
 /* exported: one ccd_descend; frozen < 0 means None */
 int orc_ccd_descend(const double *x, const double *y, int m, int d, double lam, const double *start, int frozen,
                     double sweep_tol, int max_sweeps, double *beta_out, double *obj_out, int *sweeps_out,
@@ -332,6 +153,24 @@ int orc_ccd_descend(const double *x, const double *y, int m, int d, double lam, 
 {
     if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
     orc_problem P = {x, y, m, d, lam};
+    orc_descent D;
+    if (trace_len) *trace_len = 0;
+    ccd_descend(&P, start, frozen, sweep_tol, max_sweeps, &D, NULL, trace, trace_len);
+    memcpy(beta_out, D.beta, sizeof(double) * d);
+    *obj_out = D.objective;
+    *sweeps_out = D.sweeps;
+    *steps_out = D.steps;
+    *conv_out = D.converged;
+    return 0;
+}
+
+/* exported: one ccd_descend in fp32 mode (binary32 data and descent) */
+int orc_ccd_descend_f32(const float *x, const float *y, int m, int d, double lam, const double *start, int frozen,
+                        double sweep_tol, int max_sweeps, double *beta_out, double *obj_out, int *sweeps_out,
+                        int *steps_out, int *conv_out, double *trace, int *trace_len)
+{
+    if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
+    orc_problem P = {NULL, NULL, m, d, lam, x, y, 1};
     orc_descent D;
     if (trace_len) *trace_len = 0;
     ccd_descend(&P, start, frozen, sweep_tol, max_sweeps, &D, NULL, trace, trace_len);
@@ -590,10 +429,7 @@ static int outer_search(orc_curve *c, double lo, double hi, const orc_locus_para
  * numpy uses pairwise_sum.  Measured: oracle/probe_numerics.py. */
 static double col_abs_sum(const orc_problem *P, int j)
 {
-    if (P->d == 1) return np_sum_abs(P->x, P->m);
-    double s = 0.0;
-    for (int i = 0; i < P->m; ++i) s += fabs(P->x[(size_t)i * P->d + j]);
-    return s;
+    return P->f32 ? col_abs_sum_t_f32(P, j) : col_abs_sum_t(P, j);
 }
 
 static void default_bracket(const orc_problem *P, double *lo, double *hi)
@@ -603,11 +439,7 @@ static void default_bracket(const orc_problem *P, double *lo, double *hi)
         double mean = col_abs_sum(P, j) / (double)P->m;
         if (j == 0 || mean > scale) scale = mean;
     }
-    double ymax = 0.0;
-    for (int i = 0; i < P->m; ++i) {
-        double a = fabs(P->y[i]);
-        if (i == 0 || a > ymax) ymax = a;
-    }
+    double ymax = P->f32 ? y_absmax_t_f32(P) : y_absmax_t(P);
     double radius = scale > 0 ? ymax / scale : INFINITY;
     if (!isfinite(radius) || radius <= 0) radius = 1.0;
     *lo = -radius;
@@ -797,7 +629,13 @@ static void solve_locus(const orc_problem *P, const orc_locus_params *prm, orc_l
     ccd_descend(P, best.beta, -1, prm->inner_sweep_tol, prm->inner_max_sweeps, &pol, &cnt, NULL, NULL);
     const double *beta = pol.objective <= best.value ? pol.beta : best.beta;
     memcpy(res->beta, beta, sizeof(double) * P->d);
-    res->objective = orc_objective(P->x, P->y, P->m, P->d, P->lam, res->beta);
+    if (P->f32) {
+        float bf[ORC_MAX_D];
+        for (int j = 0; j < P->d; ++j) bf[j] = (float)res->beta[j];
+        res->objective = (double)orc_objective_f32(P->xf, P->yf, P->m, P->d, (float)P->lam, bf);
+    } else {
+        res->objective = orc_objective(P->x, P->y, P->m, P->d, P->lam, res->beta);
+    }
     res->iterations = rounds;
     res->objective_evals = calls;
     res->converged = converged;
@@ -829,6 +667,7 @@ int orc_solve_locus(const double *x, const double *y, int m, int d, double lam, 
 /* batched solve across host threads (bench cpu_baseline / --impl reference) */
 typedef struct {
     const double *X, *Y, *L;
+    const float *Xf, *Yf, *Lf; /* fp32 mode */
     long long B;
     int m, d;
     double lam_floor;
@@ -848,8 +687,22 @@ static void *batch_worker(void *arg)
         long long b = bt->next++;
         pthread_mutex_unlock(&bt->mu);
         if (b >= bt->B) break;
-        double lam = bt->L[b] > bt->lam_floor ? bt->L[b] : bt->lam_floor;
-        orc_problem P = {bt->X + (size_t)b * bt->m * bt->d, bt->Y + (size_t)b * bt->m, bt->m, bt->d, lam};
+        orc_problem P;
+        memset(&P, 0, sizeof(P));
+        P.m = bt->m;
+        P.d = bt->d;
+        double lraw;
+        if (bt->Xf) {
+            P.xf = bt->Xf + (size_t)b * bt->m * bt->d;
+            P.yf = bt->Yf + (size_t)b * bt->m;
+            P.f32 = 1;
+            lraw = (double)bt->Lf[b];
+        } else {
+            P.x = bt->X + (size_t)b * bt->m * bt->d;
+            P.y = bt->Y + (size_t)b * bt->m;
+            lraw = bt->L[b];
+        }
+        P.lam = lraw > bt->lam_floor ? lraw : bt->lam_floor;
         orc_locus_result r;
         solve_locus(&P, bt->prm, &r);
         memcpy(bt->beta + (size_t)b * bt->d, r.beta, sizeof(double) * bt->d);
@@ -864,20 +717,37 @@ static void *batch_worker(void *arg)
     return NULL;
 }
 
+static int run_batch(orc_batch *bt, int nthreads)
+{
+    pthread_mutex_init(&bt->mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    pthread_t th[256];
+    if (nthreads > 256) nthreads = 256;
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, batch_worker, bt);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&bt->mu);
+    return 0;
+}
+
 int orc_solve_locus_batch(const double *X, const double *Y, const double *L, long long B, int m, int d,
                           double lam_floor, const orc_locus_params *prm, int nthreads, double *beta, double *obj,
                           int *iters, int *evals, int *conv, int *status, long long *descents, long long *steps)
 {
     if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
-    orc_batch bt = {X, Y, L, B, m, d, lam_floor, prm, beta, obj, iters, evals, conv, status, descents, steps, 0};
-    pthread_mutex_init(&bt.mu, NULL);
-    if (nthreads < 1) nthreads = 1;
-    pthread_t th[256];
-    if (nthreads > 256) nthreads = 256;
-    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, batch_worker, &bt);
-    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
-    pthread_mutex_destroy(&bt.mu);
-    return 0;
+    orc_batch bt = {X, Y, L, NULL, NULL, NULL, B, m, d, lam_floor, prm, beta, obj, iters, evals, conv, status,
+                    descents, steps, 0};
+    return run_batch(&bt, nthreads);
+}
+
+/* fp32 mode: binary32 data and descents, binary64 outer search; outputs widened */
+int orc_solve_locus_batch_f32(const float *X, const float *Y, const float *L, long long B, int m, int d,
+                              double lam_floor, const orc_locus_params *prm, int nthreads, double *beta, double *obj,
+                              int *iters, int *evals, int *conv, int *status, long long *descents, long long *steps)
+{
+    if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
+    orc_batch bt = {NULL, NULL, NULL, X, Y, L, B, m, d, lam_floor, prm, beta, obj, iters, evals, conv, status,
+                    descents, steps, 0};
+    return run_batch(&bt, nthreads);
 }
 
 /* ------------------------------------------------------------------ */

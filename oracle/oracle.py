@@ -46,8 +46,8 @@ class LocusParams(C.Structure):
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "ladlasso_oracle.c")
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+    newest = max(os.path.getmtime(os.path.join(_HERE, f)) for f in ("ladlasso_oracle.c", "orc_descent.inc"))
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
         subprocess.run(["make", "-s", "-C", _HERE, "liboracle.so"], check=True)
     return _LIB_PATH
 
@@ -76,6 +76,13 @@ def lib():
         L.orc_ccd_descend.restype = C.c_int
         L.orc_ccd_descend.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp, C.c_int, C.c_double, C.c_int,
                                       dp, dp, ip, ip, ip, dp, ip]
+        fp = C.POINTER(C.c_float)
+        L.orc_ccd_descend_f32.restype = C.c_int
+        L.orc_ccd_descend_f32.argtypes = [fp, fp, C.c_int, C.c_int, C.c_double, dp, C.c_int, C.c_double, C.c_int,
+                                          dp, dp, ip, ip, ip, dp, ip]
+        L.orc_solve_locus_batch_f32.restype = C.c_int
+        L.orc_solve_locus_batch_f32.argtypes = [fp, fp, fp, C.c_longlong, C.c_int, C.c_int, C.c_double,
+                                                C.POINTER(LocusParams), C.c_int, dp, dp, ip, ip, ip, ip, lp, lp]
         L.orc_pcg32_sequence.restype = None
         L.orc_pcg32_sequence.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_uint32)]
         L.orc_solve_locus.restype = C.c_int
@@ -97,6 +104,15 @@ def lib():
 def _d(a):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f(a):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _is_f32(*arrays):
+    return any(getattr(a, "dtype", None) == np.float32 for a in arrays)
 
 
 def np_sum(a) -> float:
@@ -153,15 +169,18 @@ class Descent:
 
 
 def ccd_descend(x, y, lam_eff, start, frozen_axis=None, sweep_tolerance=1e-10, max_sweeps=500, trace=False):
-    x, px = _d(x)
-    y, py = _d(y)
+    """float32 x/y select the fp32 mode (binary32 descent; start and outputs stay binary64)."""
+    f32 = _is_f32(x, y)
+    x, px = (_f if f32 else _d)(x)
+    y, py = (_f if f32 else _d)(y)
     s, ps = _d(start)
     m, d = x.shape
     beta = np.empty(d)
     obj = C.c_double()
     sw, st, cv, tl = C.c_int(), C.c_int(), C.c_int(), C.c_int()
     tbuf = np.empty(max_sweeps * d + 1) if trace else None
-    rc = lib().orc_ccd_descend(px, py, m, d, lam_eff, ps, -1 if frozen_axis is None else int(frozen_axis),
+    fn = lib().orc_ccd_descend_f32 if f32 else lib().orc_ccd_descend
+    rc = fn(px, py, m, d, lam_eff, ps, -1 if frozen_axis is None else int(frozen_axis),
                                sweep_tolerance, max_sweeps, beta.ctypes.data_as(C.POINTER(C.c_double)),
                                C.byref(obj), C.byref(sw), C.byref(st), C.byref(cv),
                                None if tbuf is None else tbuf.ctypes.data_as(C.POINTER(C.c_double)),
@@ -224,10 +243,13 @@ def solve_locus(x, y, lam_eff, **kw) -> LocusResult:
 
 
 def solve_locus_batch(X, Y, L, lambda_floor=1e-9, nthreads=None, **kw):
-    """Batched oracle solve over host threads; X (B,m,d), Y (B,m), L (B,) raw lambdas."""
-    X, pX = _d(X)
-    Y, pY = _d(Y)
-    L, pL = _d(L)
+    """Batched oracle solve over host threads; X (B,m,d), Y (B,m), L (B,) raw lambdas.
+    float32 X/Y select the fp32 mode (then L is taken as float32 too)."""
+    f32 = _is_f32(X, Y)
+    cv_ = _f if f32 else _d
+    X, pX = cv_(X)
+    Y, pY = cv_(Y)
+    L, pL = cv_(L)
     B, m, d = X.shape
     prm = make_params(**kw)
     nthreads = nthreads or os.cpu_count() or 1
@@ -241,7 +263,8 @@ def solve_locus_batch(X, Y, L, lambda_floor=1e-9, nthreads=None, **kw):
     stp = np.empty(B, np.int64)
     ip = C.POINTER(C.c_int)
     lp = C.POINTER(C.c_longlong)
-    rc = lib().orc_solve_locus_batch(pX, pY, pL, B, m, d, lambda_floor, C.byref(prm), nthreads,
+    fn = lib().orc_solve_locus_batch_f32 if f32 else lib().orc_solve_locus_batch
+    rc = fn(pX, pY, pL, B, m, d, lambda_floor, C.byref(prm), nthreads,
                                      beta.ctypes.data_as(C.POINTER(C.c_double)),
                                      obj.ctypes.data_as(C.POINTER(C.c_double)), it.ctypes.data_as(ip),
                                      ev.ctypes.data_as(ip), cv.ctypes.data_as(ip), stt.ctypes.data_as(ip),

@@ -14,6 +14,7 @@ from . import _build
 SYMBOLS = (
     "lad_version",
     "lad_last_error",
+    "lad_kernel_launches",
     "lad_default_params",
     "lad_set_kernel_policy",
     "lad_set_axis_parallel",
@@ -25,6 +26,10 @@ SYMBOLS = (
     "lad_objective_f64",
     "lad_generate_f64",
     "lad_subsets_f64",
+    "lad_locus_solve_f32",
+    "lad_locus_solve_host_f32",
+    "lad_ccd_descend_f32",
+    "lad_fp32_peak_tflops",
 )
 
 LAD_OK = 0
@@ -110,15 +115,26 @@ def load(build_if_missing: bool = False):
     L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams),
                                            C.POINTER(LocusOut), vp]
     L.lad_fp64_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
+    L.lad_fp32_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
+    L.lad_locus_solve_f32.argtypes = L.lad_locus_solve_f64.argtypes
+    L.lad_locus_solve_host_f32.argtypes = L.lad_locus_solve_host_f64.argtypes
     L.lad_ccd_descend_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, dbl, i32, dbl, C.POINTER(LocusOut), vp]
+    L.lad_ccd_descend_f32.argtypes = L.lad_ccd_descend_f64.argtypes
     L.lad_brute_solve_f64.argtypes = [vp, vp, vp, i64, i32, i32, i32, i64, dbl, vp, vp, vp, vp]
     L.lad_objective_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, dbl, vp, vp]
     L.lad_generate_f64.argtypes = [i32, C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp, vp]
     L.lad_subsets_f64.argtypes = [vp, vp, i32, i32, i32, i64, i64, vp, vp, vp]
-    for name in SYMBOLS[3:]:
-        getattr(L, name).restype = C.c_int
+    L.lad_kernel_launches.restype = C.c_longlong
+    for name in SYMBOLS:
+        if name not in ("lad_version", "lad_last_error", "lad_kernel_launches", "lad_default_params"):
+            getattr(L, name).restype = C.c_int
     _lib = L
     return L
+
+
+def kernel_launches() -> int:
+    """Kernels launched by the library so far (the bench's gpu_launches evidence)."""
+    return int(load().lad_kernel_launches())
 
 
 def last_error() -> str:

@@ -48,6 +48,7 @@ struct LocusArgs {
     const double *X;        // (Bd, n, p) row-major
     const double *Y;        // (Bd, n)
     const double *lam;      // (B,) raw lambda per problem
+    const float *Xf, *Yf, *lamf;  // fp32 mode inputs (warp kernel<float>); X, Y, lam unused then
     const int64_t *data_index;  // (B,) problem -> dataset row, or null (identity)
     int64_t B;
     int n, p;

@@ -15,20 +15,41 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double dfma(double a, double b, double c) { return __fma_rn(a, b, c); }
+// binary32 twins (fp32 mode: same operation order, every result rounded to binary32)
+__device__ __forceinline__ float dadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float dsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float dmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float ddiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float dfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+template <typename T>
+__device__ __forceinline__ T inf_of();
+template <>
+__device__ __forceinline__ double inf_of<double>() { return __longlong_as_double(0x7ff0000000000000LL); }
+template <>
+__device__ __forceinline__ float inf_of<float>() { return __int_as_float(0x7f800000); }
+
+template <typename T>
+struct vec2_of;
+template <>
+struct vec2_of<double> { using type = double2; };
+template <>
+struct vec2_of<float> { using type = float2; };
 
 // numpy pairwise_sum (loops_utils.h.src) over n <= 128 values produced by f(i).
 // n is a compile-time constant in the fast kernels, so the tree unrolls.
 template <typename F>
-__device__ __forceinline__ double np_sum(int n, F f)
+__device__ __forceinline__ auto np_sum(int n, F f) -> decltype(f(0))
 {
+    using T = decltype(f(0));
     if (n < 8) {
-        double res = 0.0;
+        T res = T(0);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
             if (i < n) res = dadd(res, f(i));
         return res;
     }
-    double r0 = f(0), r1 = f(1), r2 = f(2), r3 = f(3), r4 = f(4), r5 = f(5), r6 = f(6), r7 = f(7);
+    T r0 = f(0), r1 = f(1), r2 = f(2), r3 = f(3), r4 = f(4), r5 = f(5), r6 = f(6), r7 = f(7);
     int lim = n - (n % 8);
     int i = 8;
 #pragma unroll 1
@@ -36,7 +57,7 @@ __device__ __forceinline__ double np_sum(int n, F f)
         r0 = dadd(r0, f(i + 0)); r1 = dadd(r1, f(i + 1)); r2 = dadd(r2, f(i + 2)); r3 = dadd(r3, f(i + 3));
         r4 = dadd(r4, f(i + 4)); r5 = dadd(r5, f(i + 5)); r6 = dadd(r6, f(i + 6)); r7 = dadd(r7, f(i + 7));
     }
-    double res = dadd(dadd(dadd(r0, r1), dadd(r2, r3)), dadd(dadd(r4, r5), dadd(r6, r7)));
+    T res = dadd(dadd(dadd(r0, r1), dadd(r2, r3)), dadd(dadd(r4, r5), dadd(r6, r7)));
 #pragma unroll 1
     for (; i < n; ++i) res = dadd(res, f(i));
     return res;
@@ -44,15 +65,16 @@ __device__ __forceinline__ double np_sum(int n, F f)
 
 // Same tree with fully unrolled loops for a compile-time length N.
 template <int N, typename F>
-__device__ __forceinline__ double np_sum_c(F f)
+__device__ __forceinline__ auto np_sum_c(F f) -> decltype(f(0))
 {
+    using T = decltype(f(0));
     if constexpr (N < 8) {
-        double res = 0.0;
+        T res = T(0);
 #pragma unroll
         for (int i = 0; i < N; ++i) res = dadd(res, f(i));
         return res;
     } else {
-        double r[8];
+        T r[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) r[j] = f(j);
         constexpr int lim = N - (N % 8);
@@ -60,7 +82,7 @@ __device__ __forceinline__ double np_sum_c(F f)
         for (int i = 8; i < lim; i += 8)
 #pragma unroll
             for (int j = 0; j < 8; ++j) r[j] = dadd(r[j], f(i + j));
-        double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+        T res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
 #pragma unroll
         for (int i = lim; i < N; ++i) res = dadd(res, f(i));
         return res;
@@ -136,27 +158,28 @@ __device__ __forceinline__ double blas_ddot_c(FX fx, FY fy)
 // One output of x @ b through OpenBLAS dgemv_t (SkylakeX), d <= 8; `row` and
 // the row count m pick the 4x4 / 4x2 / 4x1 kernel for d == 8.  xr(j) reads x[row][j].
 template <typename FXR, typename FB>
-__device__ __forceinline__ double gemv_row(int d, int row, int m, FXR xr, FB b)
+__device__ __forceinline__ auto gemv_row(int d, int row, int m, FXR xr, FB b) -> decltype(xr(0))
 {
+    using T = decltype(xr(0));
     int nb = d & -4, m3 = d & 3;
-    double S = 0.0;
+    T S = T(0);
     if (nb == 4) {
-        double p0 = dmul(xr(0), b(0)), p1 = dmul(xr(1), b(1)), p2 = dmul(xr(2), b(2)), p3 = dmul(xr(3), b(3));
+        T p0 = dmul(xr(0), b(0)), p1 = dmul(xr(1), b(1)), p2 = dmul(xr(2), b(2)), p3 = dmul(xr(3), b(3));
         S = dadd(dadd(p0, p2), dadd(p1, p3));
     } else if (nb == 8) {
         int g4 = 4 * (m >> 2);
         if (row < g4) {
-            double q[4];
+            T q[4];
 #pragma unroll
             for (int l = 0; l < 4; ++l) q[l] = dfma(xr(l + 4), b(l + 4), dmul(xr(l), b(l)));
             S = dadd(dadd(q[0], q[2]), dadd(q[1], q[3]));
         } else {
-            double p[8];
+            T p[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) p[j] = dmul(xr(j), b(j));
             if ((m & 2) && row < g4 + 2) {
-                double L0 = dadd(dadd(dadd(p[0], p[2]), p[4]), p[6]);
-                double L1 = dadd(dadd(dadd(p[1], p[3]), p[5]), p[7]);
+                T L0 = dadd(dadd(dadd(p[0], p[2]), p[4]), p[6]);
+                T L1 = dadd(dadd(dadd(p[1], p[3]), p[5]), p[7]);
                 S = dadd(L0, L1);
             } else {
                 S = dadd(dadd(dadd(p[0], p[4]), dadd(p[2], p[6])), dadd(dadd(p[1], p[5]), dadd(p[3], p[7])));

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 
 #include "../../include/ladlasso_b200.h"
@@ -18,9 +19,10 @@
 #include "lad_locus.cuh"
 #include "lad_locus_warp.cuh"
 
-#define LAD_VERSION 101
+#define LAD_VERSION 102
 
 static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};  // kernels this library has launched (all threads)
 
 static int fail(int code, const char *fmt, ...)
 {
@@ -40,6 +42,7 @@ static int fail(int code, const char *fmt, ...)
     } while (0)
 
 extern "C" int lad_version(void) { return LAD_VERSION; }
+extern "C" long long lad_kernel_launches(void) { return g_launches.load(); }
 extern "C" const char *lad_last_error(void) { return g_err.c_str(); }
 
 extern "C" void lad_default_params(lad_locus_params *prm)
@@ -77,18 +80,27 @@ Variant make_thread_variant()
     return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double), 32, 32};
 }
 
-template <int P, int NC>
+template <int P, int NC, typename T = double>
 Variant make_warp_variant()
 {
-    return Variant{lad::locus_warp_kernel<P, NC>, 31, P, 0, 32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
+    return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, 0, 32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
 }
 
 int g_kernel_policy = LAD_KERNEL_AUTO;
 int g_axis_parallel = 1;
 
-bool pick_variant(int n, int p, Variant &v)
+bool pick_variant(int n, int p, Variant &v, bool f32)
 {
     const bool warp_ok = n <= 31 && p <= 8;
+    if (f32) {  // fp32 mode: warp-per-problem only
+        if (!warp_ok) return false;
+        if (n == 31 && p == 8) v = make_warp_variant<8, 31, float>();
+        else if (n == 30 && p == 5) v = make_warp_variant<5, 30, float>();
+        else if (p <= 3) v = make_warp_variant<3, 0, float>();
+        else if (p <= 5) v = make_warp_variant<5, 0, float>();
+        else v = make_warp_variant<8, 0, float>();
+        return true;
+    }
     const bool thread_exact = n == 10 && p == 2;  // config 1: thread-per-problem (north_star's tiny-n variant)
     int policy = g_kernel_policy;
     if (policy == LAD_KERNEL_AUTO) policy = (thread_exact || !warp_ok) ? LAD_KERNEL_THREAD : LAD_KERNEL_WARP;
@@ -123,9 +135,10 @@ int seen_capacity(const lad_locus_params *prm, int p)
     return (int)std::min<long long>(cap, 1 << 20);
 }
 
-int run_locus(const double *X, const double *Y, const double *lam, const int64_t *data_index, int64_t B, int n, int p,
+// X, Y, lam are double* (f32 == false) or float* (f32 == true)
+int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data_index, int64_t B, int n, int p,
               const lad_locus_params *prm, const lad_locus_out *out, cudaStream_t st, int mode, const double *start,
-              const int32_t *frozen, double desc_tol, int desc_sweeps)
+              const int32_t *frozen, double desc_tol, int desc_sweeps, bool f32 = false)
 {
     if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1 (got %lld, %d, %d)", (long long)B, n, p);
     if (B == 0) return LAD_OK;
@@ -142,7 +155,8 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
         return fail(LAD_E_INVALID, "bracket needs lo < hi");
     if (!(prm->lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     Variant v;
-    if (!pick_variant(n, p, v)) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+    if (!pick_variant(n, p, v, f32))
+        return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : 32);
 
     if (g_num_sms == 0) {
         int dev;
@@ -165,9 +179,15 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
 
     lad::LocusArgs A;
     memset(&A, 0, sizeof A);
-    A.X = X;
-    A.Y = Y;
-    A.lam = lam;
+    if (f32) {
+        A.Xf = (const float *)X;
+        A.Yf = (const float *)Y;
+        A.lamf = (const float *)lam;
+    } else {
+        A.X = (const double *)X;
+        A.Y = (const double *)Y;
+        A.lam = (const double *)lam;
+    }
     A.data_index = data_index;
     A.B = B;
     A.n = n;
@@ -200,17 +220,17 @@ int run_locus(const double *X, const double *Y, const double *lam, const int64_t
     cudaError_t le;
     if (!axis_par) {
         A.axis_mode = lad::AXIS_SERIAL;
-        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
+        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A); ++g_launches;
         le = cudaGetLastError();
     } else {
         A.axis_mode = lad::AXIS_SEARCH;
-        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A);
+        v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A); ++g_launches;
         le = cudaGetLastError();
         A.axis_mode = lad::AXIS_FINISH;
         A.counter = (unsigned long long *)(buf + 64);
         int64_t grid2 = std::min<int64_t>((B + v.slots_per_block - 1) / v.slots_per_block, max_grid);
         if (le == cudaSuccess) {
-            v.fn<<<(unsigned)grid2, v.block, v.smem, st>>>(A);
+            v.fn<<<(unsigned)grid2, v.block, v.smem, st>>>(A); ++g_launches;
             le = cudaGetLastError();
         }
     }
@@ -261,16 +281,44 @@ extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const doubl
                      sweep_tolerance, max_sweeps);
 }
 
-extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam,
-                                        const int64_t *data_index, int64_t Bd, int64_t B, int32_t n, int32_t p,
-                                        const lad_locus_params *prm, const lad_locus_out *out, void *stream)
+extern "C" int lad_locus_solve_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,
+                                   int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                                   const lad_locus_out *out, void *stream)
+{
+    lad_locus_params def;
+    if (!prm) {
+        lad_default_params(&def);
+        prm = &def;
+    }
+    return run_locus(X, Y, lam, data_index, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr, nullptr,
+                     0.0, 0, true);
+}
+
+extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *lam, int64_t B, int32_t n, int32_t p,
+                                   const double *start, const int32_t *frozen, double sweep_tolerance,
+                                   int32_t max_sweeps, double lambda_floor, const lad_locus_out *out, void *stream)
+{
+    if (!(sweep_tolerance > 0)) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
+    if (max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
+    if (!start) return fail(LAD_E_INVALID, "start must be non-null");
+    lad_locus_params prm;
+    lad_default_params(&prm);
+    prm.lambda_floor = lambda_floor;
+    return run_locus(X, Y, lam, nullptr, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
+                     sweep_tolerance, max_sweeps, true);
+}
+
+template <typename T>
+static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t *data_index, int64_t Bd, int64_t B,
+                            int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream)
 {
     cudaStream_t st = (cudaStream_t)stream;
     if (B < 0 || Bd < 0) return fail(LAD_E_INVALID, "B < 0");
     if (!data_index && Bd != B) return fail(LAD_E_INVALID, "Bd must equal B without data_index");
     if (B == 0) return LAD_OK;
     auto rup = [](size_t s) { return (s + 255) & ~(size_t)255; };
-    size_t bx = (size_t)Bd * n * p * 8, by = (size_t)Bd * n * 8, bl = (size_t)B * 8, bb = (size_t)B * p * 8;
+    const size_t es = sizeof(T);
+    size_t bx = (size_t)Bd * n * p * es, by = (size_t)Bd * n * es, bl = (size_t)B * es, bb = (size_t)B * p * 8;
     size_t bi = data_index ? (size_t)B * 8 : 0;
     size_t total = rup(bx) + rup(by) + rup(bl) + rup(bi) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) + 2 * rup(B) +
                    rup(B * 4) + rup(B * 8);
@@ -282,7 +330,7 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
         q += rup(sz);
         return r;
     };
-    double *dX = (double *)take(bx), *dY = (double *)take(by), *dL = (double *)take(bl);
+    T *dX = (T *)take(bx), *dY = (T *)take(by), *dL = (T *)take(bl);
     int64_t *dI = data_index ? (int64_t *)take(bi) : nullptr;
     lad_locus_out dout;
     dout.beta = (double *)take(bb);
@@ -299,7 +347,10 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
     if (e == cudaSuccess) e = cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && dI) e = cudaMemcpyAsync(dI, data_index, bi, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) rc = lad_locus_solve_f64(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
+    if (e == cudaSuccess) {
+        if constexpr (sizeof(T) == 4) rc = lad_locus_solve_f32(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
+        else rc = lad_locus_solve_f64(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
+    }
     if (e == cudaSuccess && rc == LAD_OK) {
         struct { void *h; const void *d; size_t s; } cp[] = {
             {out->beta, dout.beta, bb}, {out->objective, dout.objective, (size_t)B * 8},
@@ -317,38 +368,53 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
     return LAD_OK;
 }
 
-namespace {
-__global__ void fp64_peak_kernel(double *out, int iters)
+extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam,
+                                        const int64_t *data_index, int64_t Bd, int64_t B, int32_t n, int32_t p,
+                                        const lad_locus_params *prm, const lad_locus_out *out, void *stream)
 {
-    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9, a4 = a0 + 4e-9, a5 = a0 + 5e-9,
-           a6 = a0 + 6e-9, a7 = a0 + 7e-9;
-    const double m = 0.999999999, c = 1e-12;
-    for (int i = 0; i < iters; ++i) {
-        a0 = __fma_rn(a0, m, c); a1 = __fma_rn(a1, m, c); a2 = __fma_rn(a2, m, c); a3 = __fma_rn(a3, m, c);
-        a4 = __fma_rn(a4, m, c); a5 = __fma_rn(a5, m, c); a6 = __fma_rn(a6, m, c); a7 = __fma_rn(a7, m, c);
-    }
-    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
-    if (s == 12345.0) out[0] = s;  // keep the chain alive
+    return locus_solve_host<double>(X, Y, lam, data_index, Bd, B, n, p, prm, out, stream);
 }
-}  // namespace
 
-extern "C" int lad_fp64_peak_tflops(double *tflops, void *stream)
+extern "C" int lad_locus_solve_host_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,
+                                        int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                                        const lad_locus_out *out, void *stream)
 {
-    cudaStream_t st = (cudaStream_t)stream;
+    return locus_solve_host<float>(X, Y, lam, data_index, Bd, B, n, p, prm, out, stream);
+}
+
+namespace {
+// dense FMA throughput probe: 8 independent chains per thread
+template <typename T>
+__global__ void fma_peak_kernel(T *out, int iters)
+{
+    T a0 = T(threadIdx.x * 1e-9), a1 = a0 + T(1e-9), a2 = a0 + T(2e-9), a3 = a0 + T(3e-9), a4 = a0 + T(4e-9),
+      a5 = a0 + T(5e-9), a6 = a0 + T(6e-9), a7 = a0 + T(7e-9);
+    const T m = T(0.999999999), c = T(1e-12);
+    for (int i = 0; i < iters; ++i) {
+        a0 = lad::dfma(a0, m, c); a1 = lad::dfma(a1, m, c); a2 = lad::dfma(a2, m, c); a3 = lad::dfma(a3, m, c);
+        a4 = lad::dfma(a4, m, c); a5 = lad::dfma(a5, m, c); a6 = lad::dfma(a6, m, c); a7 = lad::dfma(a7, m, c);
+    }
+    T s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == T(12345.0)) out[0] = s;  // keep the chain alive
+}
+
+template <typename T>
+int fma_peak_tflops(double *tflops, cudaStream_t st)
+{
     if (g_num_sms == 0) {
         int dev;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int block = 256, blocks = g_num_sms * 8, iters = 1 << 14;
-    double *dout = nullptr;
-    CK(cudaMallocAsync((void **)&dout, 8, st));
+    T *dout = nullptr;
+    CK(cudaMallocAsync((void **)&dout, sizeof(T), st));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    fp64_peak_kernel<<<blocks, block, 0, st>>>(dout, iters);  // warm-up
+    fma_peak_kernel<T><<<blocks, block, 0, st>>>(dout, iters); ++g_launches;  // warm-up
     CK(cudaEventRecord(e0, st));
-    fp64_peak_kernel<<<blocks, block, 0, st>>>(dout, iters);
+    fma_peak_kernel<T><<<blocks, block, 0, st>>>(dout, iters); ++g_launches;
     CK(cudaEventRecord(e1, st));
     CK(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -359,6 +425,17 @@ extern "C" int lad_fp64_peak_tflops(double *tflops, void *stream)
     double flops = 2.0 * 8.0 * iters * (double)block * blocks;
     *tflops = flops / (ms * 1e-3) / 1e12;
     return LAD_OK;
+}
+}  // namespace
+
+extern "C" int lad_fp64_peak_tflops(double *tflops, void *stream)
+{
+    return fma_peak_tflops<double>(tflops, (cudaStream_t)stream);
+}
+
+extern "C" int lad_fp32_peak_tflops(double *tflops, void *stream)
+{
+    return fma_peak_tflops<float>(tflops, (cudaStream_t)stream);
 }
 
 namespace {
@@ -380,7 +457,7 @@ int brute_dispatch(const double *X, const double *Y, const double *lam, int64_t 
     A.vertices = vertices;
     if (C <= 4096) {
         int bs = 128;
-        lad::brute_thread_kernel<P><<<(unsigned)((B + bs - 1) / bs), bs, 0, st>>>(A);
+        lad::brute_thread_kernel<P><<<(unsigned)((B + bs - 1) / bs), bs, 0, st>>>(A); ++g_launches;
         cudaError_t le = cudaGetLastError();
         if (le != cudaSuccess) return fail(LAD_E_CUDA, "brute kernel: %s", cudaGetErrorString(le));
         return LAD_OK;
@@ -398,8 +475,8 @@ int brute_dispatch(const double *X, const double *Y, const double *lam, int64_t 
     A.partial = (lad::BruteKey *)buf;
     A.pcount = (unsigned long long *)(buf + (size_t)B * A.nchunks * sizeof(lad::BruteKey));
     dim3 grid((unsigned)A.nchunks, (unsigned)B);
-    lad::brute_chunk_kernel<P><<<grid, 256, 0, st>>>(A);
-    lad::brute_reduce_kernel<P><<<(unsigned)((B + 127) / 128), 128, 0, st>>>(A);
+    lad::brute_chunk_kernel<P><<<grid, 256, 0, st>>>(A); ++g_launches;
+    lad::brute_reduce_kernel<P><<<(unsigned)((B + 127) / 128), 128, 0, st>>>(A); ++g_launches;
     cudaError_t le = cudaGetLastError();
     cudaFreeAsync(buf, st);
     if (le != cudaSuccess) return fail(LAD_E_CUDA, "brute kernel: %s", cudaGetErrorString(le));
@@ -442,14 +519,14 @@ extern "C" int lad_objective_f64(const double *X, const double *Y, const double 
     cudaStream_t st = (cudaStream_t)stream;
     unsigned g = (unsigned)((B + 127) / 128);
     switch (p) {
-    case 1: lad::objective_kernel<1><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 2: lad::objective_kernel<2><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 3: lad::objective_kernel<3><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 4: lad::objective_kernel<4><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 5: lad::objective_kernel<5><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 6: lad::objective_kernel<6><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 7: lad::objective_kernel<7><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
-    case 8: lad::objective_kernel<8><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); break;
+    case 1: lad::objective_kernel<1><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 2: lad::objective_kernel<2><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 3: lad::objective_kernel<3><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 4: lad::objective_kernel<4><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 5: lad::objective_kernel<5><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 6: lad::objective_kernel<6><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 7: lad::objective_kernel<7><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
+    case 8: lad::objective_kernel<8><<<g, 128, 0, st>>>(X, Y, lam, B, n, beta, lambda_floor, objective); ++g_launches; break;
     }
     CK(cudaGetLastError());
     return LAD_OK;
@@ -463,7 +540,7 @@ extern "C" int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, in
     if (config == 1 && !lam) return fail(LAD_E_INVALID, "config 1 draws lambda per problem: lam must be non-null");
     if (B == 0) return LAD_OK;
     lad::GenArgs G{config, seed, first, B, n, p, X, Y, lam, beta_true};
-    lad::gen_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(G);
+    lad::gen_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(G); ++g_launches;
     CK(cudaGetLastError());
     return LAD_OK;
 }
@@ -475,7 +552,7 @@ extern "C" int lad_subsets_f64(const double *X0, const double *Y0, int32_t n0, i
     if (first < 0 || first + B > lad::binom(n0, keep)) return fail(LAD_E_INVALID, "subset index out of range");
     if (B == 0) return LAD_OK;
     lad::subsets_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(X0, Y0, n0, p, keep, first, B,
-                                                                                       X, Y);
+                                                                                       X, Y); ++g_launches;
     CK(cudaGetLastError());
     return LAD_OK;
 }

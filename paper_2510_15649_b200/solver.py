@@ -77,9 +77,22 @@ class BatchedSolveResult:
             raise InvalidInputError(f"problem {i}: non-finite data or invalid lambda")
 
 
-def _validate_host(X, y, lam):
-    X = np.ascontiguousarray(X, dtype=np.float64)
-    y = np.ascontiguousarray(y, dtype=np.float64)
+def _is_f32(X) -> bool:
+    """fp32 mode is selected by a binary32 design matrix (numpy or torch)."""
+    dt = getattr(X, "dtype", None)
+    if dt is None:
+        return False
+    if _is_torch(X):
+        import torch
+
+        return dt == torch.float32
+    return dt == np.float32
+
+
+def _validate_host(X, y, lam, f32=False):
+    ft = np.float32 if f32 else np.float64
+    X = np.ascontiguousarray(X, dtype=ft)
+    y = np.ascontiguousarray(y, dtype=ft)
     if X.ndim != 3:
         raise InvalidInputError(f"X must be 3-D (B, n, p), got shape {X.shape}")
     B, n, p = X.shape
@@ -87,15 +100,16 @@ def _validate_host(X, y, lam):
         raise InvalidInputError(f"need m >= 1 and d >= 1, got {n} x {p}")
     if y.shape != (B, n):
         raise DimensionMismatchError(f"y has shape {y.shape}, expected {(B, n)}")
-    lam = np.array(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)), dtype=np.float64)
+    lam = np.array(np.broadcast_to(np.asarray(lam, dtype=ft), (B,)), dtype=ft)
     return X, y, lam
 
 
-def _validate_device(X, y, lam, nlam=None):
+def _validate_device(X, y, lam, nlam=None, f32=False):
     import torch
 
-    if X.dtype != torch.float64 or y.dtype != torch.float64:
-        raise InvalidInputError("device inputs must be float64")
+    ft = torch.float32 if f32 else torch.float64
+    if X.dtype != ft or y.dtype != ft:
+        raise InvalidInputError("device inputs must be float64 (or float32 X and y for the fp32 mode)")
     if X.dim() != 3:
         raise InvalidInputError(f"X must be 3-D (B, n, p), got shape {tuple(X.shape)}")
     B, n, p = X.shape
@@ -103,17 +117,22 @@ def _validate_device(X, y, lam, nlam=None):
         raise DimensionMismatchError(f"y has shape {tuple(y.shape)}, expected {(B, n)}")
     nl = B if nlam is None else nlam
     if not torch.is_tensor(lam):
-        lam = torch.full((nl,), float(lam), dtype=torch.float64, device=X.device)
-    lam = lam.to(device=X.device, dtype=torch.float64).reshape(-1).expand(nl).contiguous()
+        lam = torch.full((nl,), float(lam), dtype=ft, device=X.device)
+    lam = lam.to(device=X.device, dtype=ft).reshape(-1).expand(nl).contiguous()
     return X.contiguous(), y.contiguous(), lam
 
 
 def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_floor: float = DEFAULT_LAMBDA_FLOOR,
                         data_index=None, strict: bool = False, stream=None) -> BatchedSolveResult:
-    """Batched ``solve_locus`` (locus.py:300).  Inputs numpy (host) or CUDA torch tensors."""
+    """Batched ``solve_locus`` (locus.py:300).  Inputs numpy (host) or CUDA torch tensors.
+
+    float64 inputs run the reference's arithmetic (bit-exact); a float32 X selects
+    the fp32 mode (binary32 descents, binary64 outer search; include/ladlasso_b200.h).
+    Outputs are float64 either way."""
     L = _lib.load()
     cfg = cfg if cfg is not None else LocusConfig()
     solver_id = "locus_ternary" if cfg.outer_search == "ternary" else "locus_quadrature"
+    f32 = _is_f32(X)
     if _is_torch(X):
         import torch
 
@@ -121,7 +140,7 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
             data_index = data_index.to(device=X.device, dtype=torch.int64).contiguous()
             if data_index.numel() and (int(data_index.min()) < 0 or int(data_index.max()) >= X.shape[0]):
                 raise InvalidInputError("data_index out of range")
-        X, y, lam = _validate_device(X, y, lam, None if data_index is None else data_index.shape[0])
+        X, y, lam = _validate_device(X, y, lam, None if data_index is None else data_index.shape[0], f32)
         Bd, n, p = X.shape
         B = lam.shape[0]
         prm = locus_params(cfg, lambda_floor, p)
@@ -138,12 +157,12 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
                             stt.data_ptr(), dsc.data_ptr(), stp.data_ptr())
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         t0 = time.perf_counter()
-        _check(L.lad_locus_solve_f64(X.data_ptr(), y.data_ptr(), lam.data_ptr(),
-                                     data_index.data_ptr() if data_index is not None else None, B, n, p,
-                                     C.byref(prm), C.byref(out), s))
+        fn = L.lad_locus_solve_f32 if f32 else L.lad_locus_solve_f64
+        _check(fn(X.data_ptr(), y.data_ptr(), lam.data_ptr(),
+                  data_index.data_ptr() if data_index is not None else None, B, n, p, C.byref(prm), C.byref(out), s))
         res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
     else:
-        X, y, lam0 = _validate_host(X, y, 0.0)
+        X, y, lam0 = _validate_host(X, y, 0.0, f32)
         Bd, n, p = X.shape
         if data_index is not None:
             data_index = np.ascontiguousarray(data_index, dtype=np.int64)
@@ -152,7 +171,8 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
             B = data_index.shape[0]
         else:
             B = Bd
-        lam = np.array(np.broadcast_to(np.asarray(lam, dtype=np.float64), (B,)), dtype=np.float64)
+        ft = np.float32 if f32 else np.float64
+        lam = np.array(np.broadcast_to(np.asarray(lam, dtype=ft), (B,)), dtype=ft)
         prm = locus_params(cfg, lambda_floor, p)
         beta = np.empty((B, p))
         obj = np.empty(B)
@@ -164,9 +184,9 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
         stp = np.empty(B, np.int64)
         out = _lib.LocusOut(*(a.ctypes.data for a in (beta, obj, it, ev, cv, stt, dsc, stp)))
         t0 = time.perf_counter()
-        _check(L.lad_locus_solve_host_f64(X.ctypes.data, y.ctypes.data, lam.ctypes.data,
-                                          None if data_index is None else data_index.ctypes.data, Bd, B, n, p,
-                                          C.byref(prm), C.byref(out), stream))
+        fn = L.lad_locus_solve_host_f32 if f32 else L.lad_locus_solve_host_f64
+        _check(fn(X.ctypes.data, y.ctypes.data, lam.ctypes.data, None if data_index is None else data_index.ctypes.data,
+                  Bd, B, n, p, C.byref(prm), C.byref(out), stream))
         res = BatchedSolveResult(beta, obj, it, ev, cv.astype(bool), stt, dsc, stp, solver_id,
                                  time.perf_counter() - t0)
     if strict:
@@ -184,12 +204,13 @@ def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=N
     if getattr(cfg, "line_search", "exact_median") != "exact_median":
         raise InvalidInputError("the CUDA path implements line_search='exact_median' only")
     host = not _is_torch(X)
+    f32 = _is_f32(X)
     if host:
-        X, y, lam = _validate_host(X, y, lam)
+        X, y, lam = _validate_host(X, y, lam, f32)
         dev = torch.device("cuda")
         Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
     else:
-        Xt, yt, lt = _validate_device(X, y, lam)
+        Xt, yt, lt = _validate_device(X, y, lam, None, f32)
         dev = Xt.device
     B, n, p = Xt.shape
     st = torch.as_tensor(np.asarray(start, dtype=np.float64) if not _is_torch(start) else start,
@@ -214,9 +235,9 @@ def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=N
                         stt.data_ptr(), None, None)
     s = torch.cuda.current_stream(dev).cuda_stream
     t0 = time.perf_counter()
-    _check(L.lad_ccd_descend_f64(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, st.data_ptr(), fr.data_ptr(),
-                                 float(cfg.sweep_tolerance), int(cfg.max_sweeps), float(lambda_floor),
-                                 C.byref(out), s))
+    fn = L.lad_ccd_descend_f32 if f32 else L.lad_ccd_descend_f64
+    _check(fn(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, st.data_ptr(), fr.data_ptr(),
+              float(cfg.sweep_tolerance), int(cfg.max_sweeps), float(lambda_floor), C.byref(out), s))
     res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, None, None, "ccd_plain", 0.0)
     if host:
         torch.cuda.synchronize(dev)
@@ -251,6 +272,15 @@ def solve_brute_batched(X, y, lam, max_variables: int = 6, max_candidates: int =
     if host:
         return beta.cpu().numpy(), obj.cpu().numpy(), nv.cpu().numpy()
     return beta, obj, nv
+
+
+def fp32_peak_tflops() -> float:
+    """Measured dense FFMA throughput of the current device (fp32-mode roofline denominator)."""
+    import torch
+
+    v = C.c_double()
+    _check(_lib.load().lad_fp32_peak_tflops(C.byref(v), torch.cuda.current_stream().cuda_stream))
+    return v.value
 
 
 def fp64_peak_tflops() -> float:
