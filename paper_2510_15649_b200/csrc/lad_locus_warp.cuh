@@ -40,6 +40,8 @@ struct WarpShared {
     T sa[32], sw[32], sz[32];
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
     int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
+    int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
+    float tot32[PMAX];   // per axis: binary32 total of the dense-column weights (|x_ij|, lambda)
 };
 
 template <typename T>
@@ -114,10 +116,19 @@ struct WarpAccess {
         if constexpr (sizeof(T) == 4) lraw = (double)A.lamf[pr];
         else lraw = A.lam[pr];
         ok = ok && isfinite(lraw) && lraw >= 0.0;
+        const double lam_eff = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
         __syncwarp();
+        // binary32 totals of each axis' breakpoint weights (median fast path; any order will do)
+        for (int j = 0; j < p; ++j) {
+            float wf = lane < n ? static_cast<float>(fabs(W->X[lane * p + j]))
+                                : (lane == n ? static_cast<float>(T(lam_eff)) : 0.0f);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) wf = __fadd_rn(wf, __shfl_xor_sync(FULLMASK, wf, off));
+            if (lane == 0) W->tot32[j] = wf;
+        }
         C.prob = (int64_t)pr;
         C.arank = (int)(item % div);
-        C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
+        C.lam = lam_eff;
         C.sparse_mask = mask;
         __syncwarp();
         if (!ok) {
@@ -297,6 +308,32 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
                                               uint32_t &perm_valid)
 {
     const int cnt = CNTC > 0 ? CNTC : cnt_rt;
+    // Fast path (dense columns): the weighted median is usually the same
+    // element as at this axis' previous step.  Element m is the median iff the
+    // weight of the elements ordered before it, W_below, satisfies
+    // W_below < total/2 <= W_below + w_m (in numpy's sequential cumsum).  A
+    // binary32 butterfly sum is within ~6 * 2^-24 * total of the exact value,
+    // so a decision made with a 1e-5 * total margin on both sides is the
+    // reference's decision, and it also excludes the 1e-12 * total midpoint
+    // tie.  Otherwise the full order + scan below decides.
+    T t_new;
+    bool hit = false;
+    if (cacheable) {
+        const int m = W->cand[j];
+        const T lm = shfl_t(loc, m);
+        const bool below = (loc < lm) | ((loc == lm) & (lane < m));
+        const float wf = static_cast<float>(w);
+        float wb = below ? wf : 0.0f;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) wb = __fadd_rn(wb, __shfl_xor_sync(FULLMASK, wb, off));
+        const float wm = __shfl_sync(FULLMASK, wf, m);
+        const float totf = W->tot32[j];
+        const float halff = 0.5f * totf, margf = 1e-5f * totf;
+        const bool ok = totf >= 1e-30f && totf <= 3.0e38f && wb < halff - margf && __fadd_rn(wb, wm) > halff + margf;
+        hit = __all_sync(FULLMASK, ok);
+        t_new = lm;
+    }
+    if (!hit) {
     // stable order by (location, index).  The order is unique, so if this
     // axis' permutation from its previous evaluation is still sorted under the
     // new locations it is the answer; otherwise odd-even transposition rounds
@@ -355,7 +392,9 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     const int ks = k < cnt ? k : cnt - 1;
     const T tk = shfl_t(key, ks);
     const T tk1 = shfl_t(key, ks + 1 < 32 ? ks + 1 : 31);
-    const T t_new = tie ? dmul(T(0.5), dadd(tk, tk1)) : tk;
+    t_new = tie ? dmul(T(0.5), dadd(tk, tk1)) : tk;
+    if (cacheable) W->cand[j] = __shfl_sync(FULLMASK, idx, ks);  // identical value from every lane
+    }
     if (fabs(dsub(t_new, bj)) <= dmul(T(1e-14), dadd(T(1), fabs(bj)))) return;  // ccd.py:172
     T constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
     if (have_zero) constant = dadd(constant, zsum);
@@ -528,6 +567,7 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4) locus_warp_kernel(Loc
     // may be carried across descents and problems)
     uint32_t perm_valid = 0;
     Ctl<PMAX> &C = W->C;
+    if (lane < PMAX) W->cand[lane] = 0;
     if (lane == 0) C.pc = PC_FETCH;
     __syncwarp();
     for (;;) {
