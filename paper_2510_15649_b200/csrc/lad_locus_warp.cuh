@@ -41,8 +41,13 @@ struct WarpShared {
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
     int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
-    float tot32[PMAX];   // per axis: binary32 total of the dense-column weights (|x_ij|, lambda)
+    unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
+    unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
 };
+
+// margin of the fixed-point median test, in units of 2^-30 of the total weight
+// (1.5e-5 * total; quantisation error <= 32 units, FP64 cumsum error ~1e-14 * total)
+constexpr unsigned MEDIAN_MARGIN_Q = 1u << 14;
 
 template <typename T>
 __device__ __forceinline__ T shfl_t(T v, int src) { return __shfl_sync(FULLMASK, v, src); }
@@ -118,13 +123,18 @@ struct WarpAccess {
         ok = ok && isfinite(lraw) && lraw >= 0.0;
         const double lam_eff = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
         __syncwarp();
-        // binary32 totals of each axis' breakpoint weights (median fast path; any order will do)
+        // fixed-point breakpoint weights of each axis (median fast path): any
+        // summation order will do, the test keeps a margin of 2^14 units
         for (int j = 0; j < p; ++j) {
-            float wf = lane < n ? static_cast<float>(fabs(W->X[lane * p + j]))
-                                : (lane == n ? static_cast<float>(T(lam_eff)) : 0.0f);
+            const double wd = lane < n ? (double)fabs(W->X[lane * p + j]) : (lane == n ? (double)T(lam_eff) : 0.0);
+            double tot = wd;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) wf = __fadd_rn(wf, __shfl_xor_sync(FULLMASK, wf, off));
-            if (lane == 0) W->tot32[j] = wf;
+            for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(FULLMASK, tot, off);
+            const double scale = 1073741824.0 / (tot * (1.0 + 1e-9));
+            const unsigned q = (tot > 0.0 && tot < 1e300) ? __double2uint_rz(wd * scale) : 0u;
+            W->wq[j][lane] = q;
+            const unsigned sq = __reduce_add_sync(FULLMASK, q);
+            if (lane == 0) W->halfq[j] = sq / 2u;
         }
         C.prob = (int64_t)pr;
         C.arank = (int)(item % div);
@@ -311,26 +321,23 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     // Fast path (dense columns): the weighted median is usually the same
     // element as at this axis' previous step.  Element m is the median iff the
     // weight of the elements ordered before it, W_below, satisfies
-    // W_below < total/2 <= W_below + w_m (in numpy's sequential cumsum).  A
-    // binary32 butterfly sum is within ~6 * 2^-24 * total of the exact value,
-    // so a decision made with a 1e-5 * total margin on both sides is the
-    // reference's decision, and it also excludes the 1e-12 * total midpoint
-    // tie.  Otherwise the full order + scan below decides.
+    // W_below < total/2 <= W_below + w_m (in numpy's sequential cumsum).  With
+    // the weights in 2^-30-of-total fixed point (floor, <= 32 units of error
+    // per sum) both sums are exact warp reductions, and a decision made with
+    // a 2^14-unit (1.5e-5 * total) margin on both sides is the reference's
+    // decision; it also excludes the 1e-12 * total midpoint tie.  Otherwise
+    // the full order + scan below decides.
     T t_new;
     bool hit = false;
     if (cacheable) {
         const int m = W->cand[j];
         const T lm = shfl_t(loc, m);
         const bool below = (loc < lm) | ((loc == lm) & (lane < m));
-        const float wf = static_cast<float>(w);
-        float wb = below ? wf : 0.0f;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) wb = __fadd_rn(wb, __shfl_xor_sync(FULLMASK, wb, off));
-        const float wm = __shfl_sync(FULLMASK, wf, m);
-        const float totf = W->tot32[j];
-        const float halff = 0.5f * totf, margf = 1e-5f * totf;
-        const bool ok = totf >= 1e-30f && totf <= 3.0e38f && wb < halff - margf && __fadd_rn(wb, wm) > halff + margf;
-        hit = __all_sync(FULLMASK, ok);
+        const unsigned q = W->wq[j][lane];
+        const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
+        const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
+        const unsigned hq = W->halfq[j];
+        hit = (qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q);  // exact integers: warp-uniform
         t_new = lm;
     }
     if (!hit) {
