@@ -259,6 +259,22 @@ __device__ __forceinline__ void write_invalid(const LocusArgs &A, int64_t pr, in
     if (A.steps) A.steps[pr] = 0;
 }
 
+// UnboundedDirectionError for the problem in C: counters as of the failing axis
+template <int PMAX>
+__device__ __forceinline__ void write_unbounded(const LocusArgs &A, const Ctl<PMAX> &C, int p, bool leader)
+{
+    if (!leader) return;
+    const int64_t pr = C.prob;
+    for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
+    A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
+    A.iterations[pr] = C.rounds;
+    A.objective_evals[pr] = C.calls;
+    A.converged[pr] = 0;
+    A.status[pr] = 1;
+    if (A.descents) A.descents[pr] = C.D;
+    if (A.steps) A.steps[pr] = C.S;
+}
+
 // first minimal |seen_t[k] - t| (locus.py:188-191), 8 loads in flight
 __device__ __forceinline__ int nearest_serial(const double *seen, int lim, double t)
 {
@@ -435,6 +451,11 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             C.oconv = (int)res[6 + PMAX];
             C.D += (int)res[7 + PMAX];
             C.S += (long long)res[8 + PMAX];
+            if (C.oconv < 0) {  // this axis' bracket expansion failed: raise here, as the serial scan does
+                write_unbounded<PMAX>(A, C, p, acc.leader());
+                C.pc = PC_FETCH;
+                break;
+            }
             C.pc = PC_AXIS_DONE;
             break;
         }
@@ -466,17 +487,17 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
         case PC_EX_1: C.g_lo = C.probe_v; PROBE(C.hi, PC_EX_2);
         case PC_EX_2: C.g_hi = C.probe_v; C.ex_it = 0; C.pc = PC_EX_LOOP; break;
         case PC_EX_LOOP: {
-            if (C.ex_it >= 60) {  // UnboundedDirectionError
-                int64_t pr = C.prob;
-                if (acc.leader()) {
-                for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = __longlong_as_double(0x7ff8000000000000LL);
-                A.objective[pr] = __longlong_as_double(0x7ff8000000000000LL);
-                A.iterations[pr] = C.rounds;
-                A.objective_evals[pr] = C.calls;
-                A.converged[pr] = 0;
-                A.status[pr] = 1;
-                if (A.descents) A.descents[pr] = C.D;
-                if (A.steps) A.steps[pr] = C.S;
+            if (C.ex_it >= 60) {  // UnboundedDirectionError (linesearch.py:266)
+                if (A.axis_mode == AXIS_SEARCH) {
+                    // record it; the finish pass raises it when this axis' turn comes
+                    if (acc.leader()) {
+                        double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
+                        res[6 + PMAX] = -1.0;
+                        res[7 + PMAX] = C.D;
+                        res[8 + PMAX] = (double)C.S;
+                    }
+                } else {
+                    write_unbounded<PMAX>(A, C, p, acc.leader());
                 }
                 C.pc = PC_FETCH;
                 break;

@@ -30,11 +30,34 @@ namespace lad {
 constexpr unsigned FULLMASK = 0xffffffffu;
 constexpr int WARPS_PER_BLOCK = 7;
 
+// Division by a precomputed reciprocal: q = RN(r * y), then two corrections
+// q += RN(r - q * x) * y with y = RN(1 / x).  The first makes q faithful, the
+// second is then correctly rounded (Markstein's theorem), so q == r / x in
+// round-to-nearest whenever nothing under- or overflows: |r| and |x| within
+// 2^+-450 (binary64) or 2^+-50 (binary32).  Used where shared memory holds the
+// reciprocal table (binary32, or binary64 with p <= 5).
+template <int PMAX, typename T>
+constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5;
+
+__device__ __forceinline__ bool div_operand_safe(double v)
+{
+    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
+    return hi - (573u << 20) < ((1474u - 573u) << 20);  // 2^-450 <= |v| < 2^451
+}
+__device__ __forceinline__ bool div_operand_safe(float v)
+{
+    const unsigned b = (unsigned)__float_as_int(v) & 0x7fffffffu;
+    return b - (77u << 23) < ((178u - 77u) << 23);  // 2^-50 <= |v| < 2^51
+}
+__device__ __forceinline__ double rcp_rn(double v) { return __drcp_rn(v); }
+__device__ __forceinline__ float rcp_rn(float v) { return __frcp_rn(v); }
+
 template <int PMAX, typename T>
 struct WarpShared {
     using T2 = typename vec2_of<T>::type;
     Ctl<PMAX> C;
     T X[32 * PMAX];  // row-major [i * p + j]
+    T RX[fast_div_v<PMAX, T> ? 32 * PMAX : 1];  // RN(1 / x), same layout; 1 for pad lanes
     T Y[32];
     T B[PMAX];       // beta of the running descent (warp-uniform)
     T sa[32], sw[32], sz[32];
@@ -109,7 +132,13 @@ struct WarpAccess {
             W->X[e] = v;
             ok = ok && isfinite(v);
             if (v == T(0)) mask |= 1u << (e % p);
+            if constexpr (fast_div_v<PMAX, T>) {
+                W->RX[e] = rcp_rn(v);
+                if (!div_operand_safe(v)) mask |= 1u << (e % p);  // column takes the generic path
+            }
         }
+        if constexpr (fast_div_v<PMAX, T>)
+            for (int e = n * p + lane; e < 32 * p; e += 32) W->RX[e] = T(1);
         for (int i = lane; i < n; i += 32) {
             T v = yg[i];
             W->Y[i] = v;
@@ -451,8 +480,8 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
 // NC > 0: compile-time row count (config shapes); NC == 0: runtime n_rt.
 template <int PMAX, int NC, typename T>
 __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, const T *xrow,
-                                          int n_rt, int j, T lam, bool col_sparse, T &r, T &f_cur, T &sum_abs_b,
-                                          uint32_t &perm_valid)
+                                          const T *yrow, int n_rt, int j, T lam, bool col_sparse, T &r, T &f_cur,
+                                          T &sum_abs_b, uint32_t &perm_valid)
 {
     const T INF = inf_of<T>();
     const int n = NC > 0 ? NC : n_rt;
@@ -460,9 +489,21 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
     const T xij = xrow[j];  // lanes >= n read a stale in-bounds slot, never used
     const T bj = W->B[j];
     if (!col_sparse) {
-        // np.divide then += b[j] (ccd.py:165-166).  Pad lanes divide 1/1: a zero
-        // numerator would send the whole warp through the division's slow path.
-        const T q = ddiv(row ? r : T(1), row ? xij : T(1));
+        // np.divide then += b[j] (ccd.py:165-166).  Pad lanes divide 1/1 (their
+        // result is discarded; it keeps them off the division's slow path).
+        const T rr = row ? r : T(1), xx = row ? xij : T(1);
+        T q;
+        if constexpr (fast_div_v<PMAX, T>) {
+            const T y = yrow[j];  // 1 on pad lanes
+            q = dmul(rr, y);
+            T e = dfma(-q, xx, rr);
+            q = dfma(e, y, q);
+            e = dfma(-q, xx, rr);
+            q = dfma(e, y, q);
+            if (!div_operand_safe(rr)) q = (rr == T(0)) ? dmul(rr, y) : ddiv(rr, xx);  // rare, divergent
+        } else {
+            q = ddiv(rr, xx);
+        }
         const T loc = row ? dadd(q, bj) : (lane == n ? T(0) : INF);
         const T w = row ? fabs(xij) : (lane == n ? lam : T(0));
         median_update<PMAX, (NC > 0 ? NC + 1 : 0), T>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, T(0), false,
@@ -510,6 +551,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
         r = dsub(W->Y[lane], g);
     }
     const T *xrow = W->X + lane * p;
+    const T *yrow = fast_div_v<PMAX, T> ? W->RX + lane * p : nullptr;
     const T sb = np_sum(p, [&](int q) { return fabs(W->B[q]); });
     T f_cur = dadd(warp_np_sum(fabs(r), n, lane), dmul(lam, sb));
     T f_sweep_start = f_cur, sum_abs_b = sb;
@@ -520,8 +562,8 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
         conv = 1;
     } else {
         for (;;) {
-            warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, n, j, lam, (sparse >> j) & 1u, r, f_cur, sum_abs_b,
-                                   perm_valid);
+            warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, j, lam, (sparse >> j) & 1u, r, f_cur,
+                                   sum_abs_b, perm_valid);
             ++steps;
             int jn = j + 1;
             jn += (jn == frozen);

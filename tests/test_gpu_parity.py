@@ -207,6 +207,48 @@ def test_edge_cases(oracle):
                 assert r.descents[0] == o.descents and r.steps[0] == o.steps
 
 
+@pytest.mark.parametrize("axis_parallel", [True, False])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_extreme_magnitudes_bit_exact(oracle, dtype, axis_parallel):
+    """Values outside the reciprocal-division range (|v| < 2^-450 or > 2^450 in binary64,
+    2^+-50 in binary32) take the generic division: whole problems scaled up, single columns
+    and single entries scaled down.  Rows exactly on the fit (residual 0) take the signed-zero
+    branch.  Solved problems must equal the oracle bit for bit; problems where the reference
+    raises UnboundedDirectionError (a huge column collapses the default bracket) must report
+    status 1 like the oracle."""
+    rng = np.random.default_rng(17)
+    big, small = (1e140, 1e-140) if dtype == np.float64 else (1e16, 1e-16)
+    for (n, p) in ((30, 5), (12, 3), (31, 8)):
+        B = 15
+        X = rng.standard_normal((B, n, p))
+        beta = np.zeros(p)
+        beta[0] = 2.0
+        Y = X @ beta
+        Y[:, ::4] += rng.laplace(0, 0.5, (B, (n + 3) // 4))  # most rows exactly on the fit: r == 0
+        X[0::5, :, 1] *= small          # tiny column
+        X[1::5, :, p - 1] *= big        # huge column (the reference reports an unbounded direction)
+        X[2::5, 3, 0] = small * 0.5     # one tiny entry
+        X[3::5] *= big                  # whole problem scaled up: every residual out of range
+        Y[3::5] *= big
+        X, Y = X.astype(dtype), Y.astype(dtype)
+        L = np.full(B, 0.2, dtype)
+        from paper_2510_15649_b200 import _lib
+
+        _lib.set_axis_parallel(axis_parallel)
+        try:
+            r = lad.solve_locus_batched(X, Y, L)
+        finally:
+            _lib.set_axis_parallel(True)
+        o = oracle.solve_locus_batch(X, Y, L)
+        assert np.array_equal(r.status, o["status"]), (n, p, r.status, o["status"])
+        # the work done up to the failing axis is the same as well
+        assert np.array_equal(r.steps, o["steps"]) and np.array_equal(r.descents, o["descents"])
+        ok = np.asarray(o["status"]) == 0
+        assert ok.sum() >= 12
+        assert np.array_equal(r.beta[ok], o["beta"][ok]) and np.array_equal(r.objective[ok], o["objective"][ok])
+        assert np.array_equal(r.steps[ok], o["steps"][ok]) and np.array_equal(r.descents[ok], o["descents"][ok])
+
+
 def test_device_generated_config2_against_oracle(oracle):
     """Config 2 shape at scale: device-generated bytes copied back, oracle on a sample."""
     X, Y, _ = G.generate(2, 512, seed=2024)
