@@ -78,6 +78,29 @@ template <typename T>
 __device__ __forceinline__ T shfl_down_t(T v, int d) { return __shfl_down_sync(FULLMASK, v, d); }
 template <typename T>
 __device__ __forceinline__ T shfl_xor_t(T v, int m) { return __shfl_xor_sync(FULLMASK, v, m); }
+// binary64: shuffle the two 32-bit halves explicitly (keeps the halves in
+// their registers; the generic overload lets the compiler swap them back)
+template <>
+__device__ __forceinline__ double shfl_t<double>(double v, int src)
+{
+    const int lo = __shfl_sync(FULLMASK, __double2loint(v), src);
+    const int hi = __shfl_sync(FULLMASK, __double2hiint(v), src);
+    return __hiloint2double(hi, lo);
+}
+template <>
+__device__ __forceinline__ double shfl_down_t<double>(double v, int d)
+{
+    const int lo = __shfl_down_sync(FULLMASK, __double2loint(v), d);
+    const int hi = __shfl_down_sync(FULLMASK, __double2hiint(v), d);
+    return __hiloint2double(hi, lo);
+}
+template <>
+__device__ __forceinline__ double shfl_xor_t<double>(double v, int m)
+{
+    const int lo = __shfl_xor_sync(FULLMASK, __double2loint(v), m);
+    const int hi = __shfl_xor_sync(FULLMASK, __double2hiint(v), m);
+    return __hiloint2double(hi, lo);
+}
 
 // numpy pairwise_sum of cnt values held one per lane (lane i -> element i).
 template <typename T>
