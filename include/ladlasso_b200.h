@@ -81,7 +81,8 @@ long long lad_kernel_launches(void);
 int lad_set_kernel_policy(int32_t policy);
 /* small batches (fewer problems than resident warps): run the independent
  * per-axis searches of each problem as separate work items, then combine them
- * in influence order (bit-identical; default on) */
+ * in influence order (bit-identical).  0 = off, 1 = small batches only
+ * (default), 2 = every batch. */
 int lad_set_axis_parallel(int32_t enable);
 /* fills the defaults of LocusConfig()/CcdConfig() */
 void lad_default_params(lad_locus_params *prm);

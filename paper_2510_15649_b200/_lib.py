@@ -50,9 +50,10 @@ def set_kernel_policy(policy: int) -> None:
         raise ValueError(last_error())
 
 
-def set_axis_parallel(enable: bool) -> None:
-    """Small-batch axis-parallel mode of the warp kernel (bit-identical results)."""
-    load().lad_set_axis_parallel(1 if enable else 0)
+def set_axis_parallel(enable) -> None:
+    """Axis-parallel mode of the warp kernel (bit-identical results): False/0 off,
+    True/1 for batches smaller than the resident warps (default), 2 for every batch."""
+    load().lad_set_axis_parallel(int(enable))
 
 
 class LocusParams(C.Structure):

@@ -171,7 +171,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     // Small batches leave most warps idle and are bound by one solve's latency:
     // run the independent per-axis searches as separate work items (warp kernel).
     const bool axis_par = g_axis_parallel && mode == lad::MODE_LOCUS && v.block > 32 && prm->outer_axis < 0 &&
-                          p > 1 && B < max_grid * v.slots_per_block;
+                          p > 1 && (g_axis_parallel == 2 || B < max_grid * v.slots_per_block);
     const int64_t items = axis_par ? B * p : B;
     int64_t want = (items + v.slots_per_block - 1) / v.slots_per_block;
     int64_t grid = std::min<int64_t>(want, max_grid);
@@ -243,7 +243,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
 
 extern "C" int lad_set_axis_parallel(int32_t enable)
 {
-    g_axis_parallel = enable != 0;
+    g_axis_parallel = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
     return LAD_OK;
 }
 
