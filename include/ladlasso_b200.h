@@ -88,9 +88,12 @@ int lad_set_axis_parallel(int32_t enable);
 void lad_default_params(lad_locus_params *prm);
 
 /* Batched solve_locus.  X (Bd, n, p), Y (Bd, n); lam (B,) raw lambdas;
- * data_index (B,) maps problem -> dataset row (NULL = identity, Bd = B). */
-int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index, int64_t B,
-                        int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+ * data_index (B,) maps problem -> dataset row (NULL = identity, then Bd == B).
+ * An index outside [0, Bd) marks that problem invalid (status 2); the call
+ * never synchronizes the stream. */
+int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index, int64_t Bd,
+                        int64_t B, int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out,
+                        void *stream);
 
 /* Same with HOST pointers for inputs and outputs (pinned or pageable); the
  * host<->device copies run inside the call on `stream`, which is synchronized
@@ -122,8 +125,9 @@ int lad_brute_solve_f64(const double *X, const double *Y, const double *lam, int
  * binary64 (exact widenings).  Parity: bit-exact against the oracle compiled
  * for binary32 (oracle/orc_descent.inc); distance to the fp64 reference is a
  * reported statistic, not a guarantee.  n <= 31, p <= 8 (warp kernel). */
-int lad_locus_solve_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index, int64_t B,
-                        int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+int lad_locus_solve_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index, int64_t Bd,
+                        int64_t B, int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out,
+                        void *stream);
 int lad_locus_solve_host_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,
                              int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
                              const lad_locus_out *out, void *stream);

@@ -112,7 +112,8 @@ def load(build_if_missing: bool = False):
     L.lad_default_params.restype = None
     L.lad_set_kernel_policy.argtypes = [i32]
     L.lad_set_axis_parallel.argtypes = [i32]
-    L.lad_locus_solve_f64.argtypes = [vp, vp, vp, vp, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut), vp]
+    L.lad_locus_solve_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams), C.POINTER(LocusOut),
+                                      vp]
     L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams),
                                            C.POINTER(LocusOut), vp]
     L.lad_fp64_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]

@@ -50,6 +50,7 @@ struct LocusArgs {
     const double *lam;      // (B,) raw lambda per problem
     const float *Xf, *Yf, *lamf;  // fp32 mode inputs (warp kernel<float>); X, Y, lam unused then
     const int64_t *data_index;  // (B,) problem -> dataset row, or null (identity)
+    int64_t Bd;                 // dataset rows (bounds of data_index; an index outside -> status 2)
     int64_t B;
     int n, p;
     LocusParamsDev prm;
@@ -321,6 +322,12 @@ struct ThreadAccess {
         C.prob = (int64_t)pr;
         C.arank = (int)(item % div);
         int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
+        if (src < 0 || src >= A.Bd) {  // data_index out of range: invalid input
+            C.lam = A.prm.lambda_floor;
+            C.sparse_mask = 0;
+            write_invalid<PMAX>(A, (int64_t)pr, p);
+            return 0;
+        }
         const double *xg = A.X + (size_t)src * n * p;
         const double *yg = A.Y + (size_t)src * n;
         bool ok = true;

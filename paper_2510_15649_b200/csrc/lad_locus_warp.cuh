@@ -138,6 +138,14 @@ struct WarpAccess {
         if ((int64_t)item >= A.B * div) return -1;
         const unsigned long long pr = item / div;
         int64_t src = A.data_index ? A.data_index[pr] : (int64_t)pr;
+        if (src < 0 || src >= A.Bd) {  // data_index out of range: invalid input (warp-uniform)
+            __syncwarp();
+            C.prob = (int64_t)pr;
+            C.arank = (int)(item % div);
+            __syncwarp();
+            if (lane == 0) write_invalid<PMAX>(A, (int64_t)pr, p);
+            return 0;
+        }
         const T *xsrc, *ysrc;
         if constexpr (sizeof(T) == 4) {
             xsrc = A.Xf;

@@ -136,12 +136,14 @@ int seen_capacity(const lad_locus_params *prm, int p)
 }
 
 // X, Y, lam are double* (f32 == false) or float* (f32 == true)
-int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data_index, int64_t B, int n, int p,
+int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data_index, int64_t Bd, int64_t B, int n, int p,
               const lad_locus_params *prm, const lad_locus_out *out, cudaStream_t st, int mode, const double *start,
               const int32_t *frozen, double desc_tol, int desc_sweeps, bool f32 = false)
 {
     if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1 (got %lld, %d, %d)", (long long)B, n, p);
     if (B == 0) return LAD_OK;
+    if (data_index && Bd < 1) return fail(LAD_E_INVALID, "Bd must be >= 1 with data_index");
+    if (!data_index && Bd != B) return fail(LAD_E_INVALID, "Bd must equal B without data_index");
     if (!out || !out->beta || !out->objective || !out->iterations || !out->objective_evals || !out->converged ||
         !out->status)
         return fail(LAD_E_INVALID, "output pointers must be non-null");
@@ -189,6 +191,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
         A.lam = (const double *)lam;
     }
     A.data_index = data_index;
+    A.Bd = data_index ? Bd : B;
     A.B = B;
     A.n = n;
     A.p = p;
@@ -255,7 +258,7 @@ extern "C" int lad_set_kernel_policy(int32_t policy)
 }
 
 extern "C" int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
-                                   int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                                   int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
                                    const lad_locus_out *out, void *stream)
 {
     lad_locus_params def;
@@ -263,8 +266,8 @@ extern "C" int lad_locus_solve_f64(const double *X, const double *Y, const doubl
         lad_default_params(&def);
         prm = &def;
     }
-    return run_locus(X, Y, lam, data_index, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr, nullptr,
-                     0.0, 0);
+    return run_locus(X, Y, lam, data_index, Bd, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr,
+                     nullptr, 0.0, 0);
 }
 
 extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
@@ -277,12 +280,12 @@ extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const doubl
     lad_locus_params prm;
     lad_default_params(&prm);
     prm.lambda_floor = lambda_floor;
-    return run_locus(X, Y, lam, nullptr, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
+    return run_locus(X, Y, lam, nullptr, B, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
                      sweep_tolerance, max_sweeps);
 }
 
 extern "C" int lad_locus_solve_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,
-                                   int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
+                                   int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
                                    const lad_locus_out *out, void *stream)
 {
     lad_locus_params def;
@@ -290,8 +293,8 @@ extern "C" int lad_locus_solve_f32(const float *X, const float *Y, const float *
         lad_default_params(&def);
         prm = &def;
     }
-    return run_locus(X, Y, lam, data_index, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr, nullptr,
-                     0.0, 0, true);
+    return run_locus(X, Y, lam, data_index, Bd, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr,
+                     nullptr, 0.0, 0, true);
 }
 
 extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *lam, int64_t B, int32_t n, int32_t p,
@@ -304,7 +307,7 @@ extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *
     lad_locus_params prm;
     lad_default_params(&prm);
     prm.lambda_floor = lambda_floor;
-    return run_locus(X, Y, lam, nullptr, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
+    return run_locus(X, Y, lam, nullptr, B, B, n, p, &prm, out, (cudaStream_t)stream, lad::MODE_DESCENT, start, frozen,
                      sweep_tolerance, max_sweeps, true);
 }
 
@@ -348,8 +351,8 @@ static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t 
     if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && dI) e = cudaMemcpyAsync(dI, data_index, bi, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
-        if constexpr (sizeof(T) == 4) rc = lad_locus_solve_f32(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
-        else rc = lad_locus_solve_f64(dX, dY, dL, dI, B, n, p, prm, &dout, stream);
+        if constexpr (sizeof(T) == 4) rc = lad_locus_solve_f32(dX, dY, dL, dI, Bd, B, n, p, prm, &dout, stream);
+        else rc = lad_locus_solve_f64(dX, dY, dL, dI, Bd, B, n, p, prm, &dout, stream);
     }
     if (e == cudaSuccess && rc == LAD_OK) {
         struct { void *h; const void *d; size_t s; } cp[] = {

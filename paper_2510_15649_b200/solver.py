@@ -136,10 +136,8 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
     if _is_torch(X):
         import torch
 
-        if data_index is not None:
-            data_index = data_index.to(device=X.device, dtype=torch.int64).contiguous()
-            if data_index.numel() and (int(data_index.min()) < 0 or int(data_index.max()) >= X.shape[0]):
-                raise InvalidInputError("data_index out of range")
+        if data_index is not None:  # bounds are checked in the kernel (status 2): no host sync here
+            data_index = torch.as_tensor(data_index, device=X.device).to(torch.int64).reshape(-1).contiguous()
         X, y, lam = _validate_device(X, y, lam, None if data_index is None else data_index.shape[0], f32)
         Bd, n, p = X.shape
         B = lam.shape[0]
@@ -159,7 +157,8 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
         t0 = time.perf_counter()
         fn = L.lad_locus_solve_f32 if f32 else L.lad_locus_solve_f64
         _check(fn(X.data_ptr(), y.data_ptr(), lam.data_ptr(),
-                  data_index.data_ptr() if data_index is not None else None, B, n, p, C.byref(prm), C.byref(out), s))
+                  data_index.data_ptr() if data_index is not None else None, Bd, B, n, p, C.byref(prm), C.byref(out),
+                  s))
         res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
     else:
         X, y, lam0 = _validate_host(X, y, 0.0, f32)

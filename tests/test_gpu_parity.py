@@ -207,6 +207,29 @@ def test_edge_cases(oracle):
                 assert r.descents[0] == o.descents and r.steps[0] == o.steps
 
 
+@pytest.mark.parametrize("policy", ["thread", "warp"])
+def test_data_index_out_of_range_is_per_problem_invalid(policy):
+    """Device data_index is bounds-checked in the kernel (no host sync): bad rows get status 2."""
+    from paper_2510_15649_b200 import _lib
+
+    g = load_golden("cfg1" if policy == "thread" else "cfg0")
+    X = torch.from_numpy(g["x"][:4]).cuda()
+    Y = torch.from_numpy(g["y"][:4]).cuda()
+    idx = torch.tensor([0, 3, -1, 4, 2, 1 << 40], device="cuda")
+    L = torch.from_numpy(np.repeat(g["lam"][:1], 6)).cuda()
+    _lib.set_kernel_policy({"thread": _lib.KERNEL_THREAD, "warp": _lib.KERNEL_WARP}[policy])
+    try:
+        r = lad.solve_locus_batched(X, Y, L, data_index=idx)
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_kernel_policy(_lib.KERNEL_AUTO)
+    assert _np(r.status).tolist() == [0, 0, 2, 2, 0, 2]
+    ref = lad.solve_locus_batched(g["x"][[0, 3, 2]], g["y"][[0, 3, 2]], np.repeat(g["lam"][:1], 3))
+    assert np.array_equal(_np(r.objective)[[0, 1, 4]], ref.objective)
+    with pytest.raises(lad.InvalidInputError):
+        lad.solve_locus_batched(X, Y, L, data_index=idx, strict=True)
+
+
 @pytest.mark.parametrize("axis_parallel", [True, False])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_extreme_magnitudes_bit_exact(oracle, dtype, axis_parallel):
