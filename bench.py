@@ -356,6 +356,14 @@ def main():
     h2d = host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes + (hidx_np.nbytes if hidx_np is not None else 0)
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
 
+    # DRAM traffic per launch from the committed ncu --set full capture of this workload (None otherwise)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"config{a.config}_{a.dtype}")
+        if tr:
+            traffic = tr["bytes_per_solve"] * solves_per_step
+    except (OSError, ValueError):
+        pass
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -397,7 +405,8 @@ def main():
                        "kernel": "thread-per-problem sm_100a" if a.config == 1 else "warp-per-problem sm_100a",
                        "l2": "flushed between steps (256 MiB memset)"},
             "roofline": {"bound": "fp64" if a.dtype == "f64" else "fp32", "achieved": achieved_tflops, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None, "traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per solve x solves per launch)",
                          "peak_source": (f"measured {'DFMA' if a.dtype == 'f64' else 'FFMA'} loop on this GPU "
                                          f"(lad_{a.dtype.replace('f', 'fp')}_peak_tflops); "
                                          "MEASURED_PEAKS.json has no FP64/FP32 CUDA-core figure"),
