@@ -13,6 +13,7 @@
  *   lad_ccd_descend_f64     <- ccd.ccd_descend(spec, start, cfg)   ccd.py:126-206
  *   lad_brute_solve_f64     <- brute.solve_brute(spec, ...)        brute.py:106-145
  *   lad_objective_f64       <- model.evaluate_objective(spec, b)   model.py:151-154
+ *   lad_axiswise_minimum_f64 <- ccd.is_axiswise_minimum(spec, b)   ccd.py:214-237
  *   lad_generate_f64        <- (no reference counterpart) device-side generation
  *                              of the BASELINE.json config problems
  *
@@ -139,6 +140,14 @@ int lad_ccd_descend_f32(const float *X, const float *Y, const float *lam, int64_
  * current device (TFLOP/s, 2 flops per FMA), timed with CUDA events on `stream`. */
 int lad_fp64_peak_tflops(double *tflops, void *stream);
 int lad_fp32_peak_tflops(double *tflops, void *stream);
+
+/* Batched ccd.is_axiswise_minimum (ccd.py:214-237): out[i] = 1 iff no
+ * axis-parallel move from beta (B, p) descends, except along skip[i] (-1 or
+ * NULL = none); 0 otherwise; 2 for non-finite inputs.  tol as the reference
+ * (1e-9, relative to max(1, |b_j|)). */
+int lad_axiswise_minimum_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                             const double *beta, const int32_t *skip, double tol, double lambda_floor, uint8_t *out,
+                             void *stream);
 
 /* evaluate_objective for (B, p) coefficient vectors. */
 int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,

@@ -454,6 +454,70 @@ def gen_cli(pool):
     print("wrote cli.json")
 
 
+def gen_curve(pool):
+    """Certificate and locus-sampling goldens: ccd.is_axiswise_minimum (ccd.py:214-237) on certified,
+    nudged and random coefficient vectors (with and without skip); locus.sample_locus (locus.py:126-147)."""
+    _ref()
+    from ladlasso.ccd import is_axiswise_minimum, solve_ccd
+    from ladlasso.datagen import GenSpec, generate
+    from ladlasso.linesearch import Bracket
+    from ladlasso.locus import default_bracket, default_outer_axis, locus_value, sample_locus
+    from ladlasso.model import ProblemSpec
+
+    rng = np.random.default_rng(2024)
+    Mx, Dx = 30, 5
+    cx, cy, cl, cb, cs, cok = [], [], [], [], [], []
+    for k in range(60):
+        d = 1 + k % Dx
+        m = 4 + (k * 7) % (Mx - 3)
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.2, seed=7000 + k))
+        lam = (0.01, 0.1, 1.0)[k % 3]
+        spec = ProblemSpec(data, lam)
+        base = solve_ccd(spec).beta.beta
+        axis = default_outer_axis(data)
+        lp = locus_value(spec, axis, float(base[axis]) + 0.3).beta.beta
+        cands = [(base, -1), (base + np.where(np.arange(d) == k % d, 1e-5 * (1 + abs(base[k % d])), 0.0), -1),
+                 (base + np.where(np.arange(d) == k % d, 1e-12, 0.0), -1), (lp, axis), (lp, -1),
+                 (rng.standard_normal(d), -1)]
+        for b, sk in cands:
+            X = np.zeros((Mx, Dx)); X[:m, :d] = data.x
+            Y = np.zeros(Mx); Y[:m] = data.y
+            B = np.zeros(Dx); B[:d] = b
+            cx.append(X); cy.append(Y); cl.append(lam); cb.append(B); cs.append(sk)
+            cok.append(bool(is_axiswise_minimum(spec, b, skip=None if sk < 0 else sk)))
+    nm = [4 + (k * 7) % (Mx - 3) for k in range(60) for _ in range(6)]
+    nd = [1 + k % Dx for k in range(60) for _ in range(6)]
+    out = dict(x=np.array(cx), y=np.array(cy), lam=np.array(cl), beta=np.array(cb), skip=np.array(cs),
+               m=np.array(nm), d=np.array(nd), certified=np.array(cok))
+    # sample_locus on 16 problems (d = 2..4), 9 or 33 points, over the default bracket or a window
+    sx, sy, sl, sm, sd, sa, sbr, sn = [], [], [], [], [], [], [], []
+    st, sbeta, sval, sconv, sev = [], [], [], [], []
+    for k in range(16):
+        d = 2 + k % 3
+        m = 6 + k % 9
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.2, seed=8000 + k))
+        spec = ProblemSpec(data, (0.01, 0.1, 1.0)[k % 3])
+        axis = default_outer_axis(data)
+        br = default_bracket(data) if k % 2 == 0 else Bracket(-0.5, 1.5)
+        npts = 9 if k % 2 else 33
+        pts = sample_locus(spec, axis, br, npts)
+        X = np.zeros((16, 4)); X[:m, :d] = data.x
+        Y = np.zeros(16); Y[:m] = data.y
+        sx.append(X); sy.append(Y); sl.append(spec.lam); sm.append(m); sd.append(d); sa.append(axis)
+        sbr.append((br.lo, br.hi)); sn.append(npts)
+        T = np.full(33, np.nan); T[:npts] = [pt.t for pt in pts]
+        Bt = np.full((33, 4), np.nan); Bt[:npts, :d] = [pt.beta.beta for pt in pts]
+        V = np.full(33, np.nan); V[:npts] = [pt.value for pt in pts]
+        Cv = np.zeros(33, bool); Cv[:npts] = [pt.inner_converged for pt in pts]
+        Ev = np.zeros(33, int); Ev[:npts] = [pt.inner_evals for pt in pts]
+        st.append(T); sbeta.append(Bt); sval.append(V); sconv.append(Cv); sev.append(Ev)
+    out.update(s_x=np.array(sx), s_y=np.array(sy), s_lam=np.array(sl), s_m=np.array(sm), s_d=np.array(sd),
+               s_axis=np.array(sa), s_bracket=np.array(sbr), s_n=np.array(sn), s_t=np.array(st),
+               s_beta=np.array(sbeta), s_value=np.array(sval), s_conv=np.array(sconv), s_evals=np.array(sev))
+    np.savez_compressed(os.path.join(GOLDEN, "curve.npz"), **out)
+    print("wrote curve.npz", int(np.sum(out["certified"])), "of", len(out["certified"]), "certified")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count())
@@ -465,7 +529,7 @@ def main():
     with Pool(a.procs) as pool:
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
-                         ("cli", gen_cli)):
+                         ("cli", gen_cli), ("curve", gen_curve)):
             if only is None or name in only:
                 fn(pool)
 

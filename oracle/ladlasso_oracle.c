@@ -182,6 +182,51 @@ int orc_ccd_descend_f32(const float *x, const float *y, int m, int d, double lam
     return 0;
 }
 
+/* ccd.is_axiswise_minimum (ccd.py:214-237) through model.axis_restriction
+ * (model.py:157-177) and PiecewiseLinear1D.slopes_at (linesearch.py:65-77):
+ * masked weight sums are numpy pairwise sums over the compacted arrays. */
+int orc_is_axiswise_minimum(const double *x, const double *y, int m, int d, double lam, const double *b, int skip,
+                            double tol)
+{
+    if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
+    double r[ORC_MAX_M];
+    residual_init(x, y, m, d, b, r);
+    for (int j = 0; j < d; ++j) {
+        if (j == skip) continue;
+        double loc[ORC_MAX_M + 1], w[ORC_MAX_M + 1], sel[ORC_MAX_M + 1];
+        int cnt = 0;
+        for (int i = 0; i < m; ++i) {
+            double c = x[(size_t)i * d + j];
+            double base = r[i] + c * b[j];
+            if (c != 0.0) {
+                loc[cnt] = base / c;
+                w[cnt] = fabs(c);
+                ++cnt;
+            }
+        }
+        loc[cnt] = 0.0;
+        w[cnt] = lam;
+        ++cnt;
+        double total = orc_np_sum(w, cnt);
+        double atol = tol * fmax(1.0, fabs(b[j]));
+        double lo = b[j] - atol, hi = b[j] + atol;
+        int nb = 0;
+        for (int q = 0; q < cnt; ++q)
+            if (loc[q] < lo) sel[nb++] = w[q];
+        double w_below = orc_np_sum(sel, nb);
+        int na = 0;
+        for (int q = 0; q < cnt; ++q)
+            if (loc[q] > hi) sel[na++] = w[q];
+        double w_above = orc_np_sum(sel, na);
+        double w_at = total - w_below - w_above;
+        double left = w_below - w_at - w_above;
+        double right = w_below + w_at - w_above;
+        double eps = 1e-12 * (total + 1.0);
+        if (left > eps || right < -eps) return 0;
+    }
+    return 1;
+}
+
 /* ------------------------------------------------------------------ */
 /* PCG32 (rng.py:25-46)                                                 */
 /* ------------------------------------------------------------------ */

@@ -83,6 +83,8 @@ def lib():
         L.orc_solve_locus_batch_f32.restype = C.c_int
         L.orc_solve_locus_batch_f32.argtypes = [fp, fp, fp, C.c_longlong, C.c_int, C.c_int, C.c_double,
                                                 C.POINTER(LocusParams), C.c_int, dp, dp, ip, ip, ip, ip, lp, lp]
+        L.orc_is_axiswise_minimum.restype = C.c_int
+        L.orc_is_axiswise_minimum.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp, C.c_int, C.c_double]
         L.orc_pcg32_sequence.restype = None
         L.orc_pcg32_sequence.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_uint32)]
         L.orc_solve_locus.restype = C.c_int
@@ -189,6 +191,17 @@ def ccd_descend(x, y, lam_eff, start, frozen_axis=None, sweep_tolerance=1e-10, m
         raise ValueError("problem shape outside oracle limits")
     return Descent(beta, obj.value, sw.value, st.value, bool(cv.value),
                    None if tbuf is None else tbuf[: tl.value].copy())
+
+
+def is_axiswise_minimum(x, y, lam_eff, beta, skip=None, tol=1e-9) -> bool:
+    x, px = _d(x)
+    y, py = _d(y)
+    b, pb = _d(beta)
+    rc = lib().orc_is_axiswise_minimum(px, py, x.shape[0], x.shape[1], lam_eff, pb, -1 if skip is None else int(skip),
+                                       tol)
+    if rc < 0:
+        raise ValueError("problem shape outside oracle limits")
+    return bool(rc)
 
 
 def pcg32_sequence(seed, n, stream=54):

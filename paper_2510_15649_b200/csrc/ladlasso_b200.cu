@@ -15,6 +15,7 @@
 
 #include "../../include/ladlasso_b200.h"
 #include "lad_brute.cuh"
+#include "lad_cert.cuh"
 #include "lad_gen.cuh"
 #include "lad_locus.cuh"
 #include "lad_locus_warp.cuh"
@@ -557,5 +558,21 @@ extern "C" int lad_subsets_f64(const double *X0, const double *Y0, int32_t n0, i
     lad::subsets_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(X0, Y0, n0, p, keep, first, B,
                                                                                        X, Y); ++g_launches;
     CK(cudaGetLastError());
+    return LAD_OK;
+}
+
+extern "C" int lad_axiswise_minimum_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
+                                        int32_t p, const double *beta, const int32_t *skip, double tol,
+                                        double lambda_floor, uint8_t *out, void *stream)
+{
+    if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1");
+    if (n > 32 || p > 8) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+    if (!(tol >= 0)) return fail(LAD_E_INVALID, "tol must be >= 0");
+    if (!(lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
+    if (B == 0) return LAD_OK;
+    lad::CertArgs A{X, Y, lam, beta, skip, B, n, p, tol, lambda_floor, out};
+    lad::axiswise_minimum_kernel<32, 8><<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(A); ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LAD_E_CUDA, "certificate kernel: %s", cudaGetErrorString(e));
     return LAD_OK;
 }

@@ -313,6 +313,41 @@ def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT
     return out.cpu().numpy() if host else out
 
 
+def axiswise_minimum_batched(X, y, lam, beta, skip=None, tol: float = 1e-9, *,
+                             lambda_floor: float = DEFAULT_LAMBDA_FLOOR):
+    """Batched ``is_axiswise_minimum`` (ccd.py:214) on the device: bool per problem.
+
+    ``skip``: None, one axis for all problems, or (B,) axes (-1 = none)."""
+    import torch
+
+    L = _lib.load()
+    host = not _is_torch(X)
+    if host:
+        X, y, lam = _validate_host(X, y, lam)
+        dev = torch.device("cuda")
+        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
+    else:
+        Xt, yt, lt = _validate_device(X, y, lam)
+        dev = Xt.device
+    B, n, p = Xt.shape
+    bt = torch.as_tensor(beta if _is_torch(beta) else np.array(beta, dtype=np.float64), dtype=torch.float64,
+                         device=dev).reshape(-1, p).expand(B, p).contiguous()
+    sk = None
+    if skip is not None:
+        sk = torch.as_tensor(skip if _is_torch(skip) else np.asarray(skip), device=dev).to(torch.int32)
+        sk = sk.reshape(-1).expand(B).contiguous()
+    out = torch.empty(B, dtype=torch.uint8, device=dev)
+    _check(L.lad_axiswise_minimum_f64(Xt.data_ptr(), yt.data_ptr(), lt.data_ptr(), B, n, p, bt.data_ptr(),
+                                      None if sk is None else sk.data_ptr(), float(tol), float(lambda_floor),
+                                      out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    if host:
+        o = out.cpu().numpy()
+        if (o == 2).any():
+            raise InvalidInputError(f"problem {int(np.nonzero(o == 2)[0][0])}: non-finite input")
+        return o == 1
+    return out == 1
+
+
 # ---------------------------------------------------------------------------
 # single-problem mirrors of the reference API (B = 1 calls)
 # ---------------------------------------------------------------------------
@@ -452,3 +487,13 @@ def evaluate_objective(spec, beta) -> float:
     if b.shape != (X.shape[2],):
         raise DimensionMismatchError(f"beta has shape {b.shape}, problem has {X.shape[2]} variables")
     return float(evaluate_objective_batched(X, y, lam, b[None], lambda_floor=floor)[0])
+
+
+def is_axiswise_minimum(spec, beta, skip=None, tol: float = 1e-9) -> bool:
+    """Drop-in for ``ladlasso.ccd.is_axiswise_minimum`` (runs on the GPU)."""
+    X, y, lam, floor = _spec_arrays(spec)
+    b = beta.beta if hasattr(beta, "beta") else np.asarray(beta, dtype=float)
+    if b.shape != (X.shape[2],):
+        raise DimensionMismatchError(f"beta has shape {b.shape}, problem has {X.shape[2]} variables")
+    return bool(axiswise_minimum_batched(X, y, lam, b[None], -1 if skip is None else int(skip), tol,
+                                         lambda_floor=floor)[0])

@@ -172,3 +172,14 @@ def test_numerics_model_matches_live_numpy():
         pytest.skip(f"order model measured for OpenBLAS SkylakeX kernels, host uses {P.openblas_arch()}")
     res = P.check(trials=10)
     assert all(v == 0 for v in res.values()), res
+
+
+def test_certificate_oracle_matches_reference(oracle):
+    """ccd.is_axiswise_minimum (ccd.py:214-237) restated: 360 certified / nudged / random vectors."""
+    g = load_golden("curve")
+    for i in range(len(g["lam"])):
+        m, d = int(g["m"][i]), int(g["d"][i])
+        sk = int(g["skip"][i])
+        got = oracle.is_axiswise_minimum(g["x"][i, :m, :d], g["y"][i, :m], max(float(g["lam"][i]), 1e-9),
+                                         g["beta"][i, :d], None if sk < 0 else sk)
+        assert got == bool(g["certified"][i]), i
