@@ -14,6 +14,7 @@
  *   lad_brute_solve_f64     <- brute.solve_brute(spec, ...)        brute.py:106-145
  *   lad_objective_f64       <- model.evaluate_objective(spec, b)   model.py:151-154
  *   lad_axiswise_minimum_f64 <- ccd.is_axiswise_minimum(spec, b)   ccd.py:214-237
+ *   lad_lp_solve_f64        <- lp.solve_lp(spec, SimplexConfig)    lp.py:106-215
  *   lad_generate_f64        <- (no reference counterpart) device-side generation
  *                              of the BASELINE.json config problems
  *
@@ -148,6 +149,23 @@ int lad_fp32_peak_tflops(double *tflops, void *stream);
 int lad_axiswise_minimum_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
                              const double *beta, const int32_t *skip, double tol, double lambda_floor, uint8_t *out,
                              void *stream);
+
+/* Batched lp.solve_lp (lp.py:106-215): dense tableau simplex on the standard
+ * form (bp, bn, rp, rn) from the sign-split residual basis.  pivot_rule:
+ * LAD_PIVOT_DANTZIG_BLAND (Dantzig, permanent switch to Bland after n
+ * degenerate pivots; default) or LAD_PIVOT_BLAND; max_pivots 0 = 50 * (2p+2n)
+ * columns.  Outputs: beta (B, p), objective = evaluate_objective(beta), pivots,
+ * converged; status 0 ok, 1 unbounded direction (SimplexError in
+ * simplex_minimize), 2 invalid input, 3 the LP optimum does not reproduce the
+ * objective within 1e-9 (SimplexError in simplex_solve).
+ * x_full (B, 2p+2n), basis (B, n) and trace (B, trace_cap: the LP objective
+ * after 0, 1, ... pivots, SimplexSolution.objective_trace) are optional (NULL). */
+#define LAD_PIVOT_DANTZIG_BLAND 0
+#define LAD_PIVOT_BLAND 1
+int lad_lp_solve_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                     int32_t max_pivots, int32_t pivot_rule, double feasibility_tolerance, double lambda_floor,
+                     double *beta, double *objective, int32_t *pivots, uint8_t *converged, uint8_t *status,
+                     double *x_full, int32_t *basis, double *trace, int32_t trace_cap, void *stream);
 
 /* evaluate_objective for (B, p) coefficient vectors. */
 int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,

@@ -423,11 +423,16 @@ def gen_cli(pool):
         with open(path) as fh:
             fx["solve_csv"] = fh.read()
         fx["solve"] = []
-        for solver in ("locus_ternary", "locus_quadrature", "brute", "ccd_plain"):
+        for solver in ("locus_ternary", "locus_quadrature", "brute", "ccd_plain", "lp"):
             for lam in ("0.05", "1.5"):
                 argv = ["solve", path, "--lambda", lam, "--solver", solver]
                 code, so, _ = _run_ref_cli(argv)
                 fx["solve"].append(dict(argv=argv[2:], code=code, stdout=so))
+        # solve --dump-lp: the exported standard form
+        lp_path = os.path.join(tmp, "s.lp")
+        _run_ref_cli(["solve", path, "--lambda", "0.3", "--solver", "lp", "--dump-lp", lp_path])
+        with open(lp_path) as fh:
+            fx["dump_lp"] = fh.read()
         # check: per-instance CSV of a small seeded sweep
         fx["check"] = []
         for argv in (["--n-instances", "16", "--seed", "5"],
@@ -444,7 +449,7 @@ def gen_cli(pool):
         # bench: runs + medians CSVs (no lp)
         out = os.path.join(tmp, "b.csv")
         argv = ["--d", "1,2,3", "--m", "6,10", "--repeats", "2", "--seed", "4",
-                "--solvers", "brute,locus_ternary,locus_quadrature,ccd_plain"]
+                "--solvers", "lp,brute,locus_ternary,locus_quadrature,ccd_plain"]
         code, so, _ = _run_ref_cli(["bench"] + argv + ["--out", out])
         with open(out) as fh, open(os.path.join(tmp, "b_medians.csv")) as fm:
             fx["bench"] = dict(argv=argv, code=code, csv=fh.read(), medians=fm.read())
@@ -518,6 +523,56 @@ def gen_curve(pool):
     print("wrote curve.npz", int(np.sum(out["certified"])), "of", len(out["certified"]), "certified")
 
 
+def gen_lp(pool):
+    """lp.solve_lp / simplex_minimize goldens (lp.py:106-215): shapes m 2..32, d 1..8, both pivot rules,
+    pivot budgets, the objective trace; dump_lp text (lp.py:218-251)."""
+    import tempfile
+
+    _ref()
+    from ladlasso.datagen import GenSpec, generate
+    from ladlasso.lp import SimplexConfig, dump_lp, formulate, simplex_minimize, solve_lp
+    from ladlasso.model import ProblemSpec
+
+    rng = np.random.default_rng(77)
+    Mx, Dx, Nx, Tx = 32, 8, 80, 64
+    rec = {k: [] for k in ("x", "y", "lam", "m", "d", "rule", "max_pivots", "beta", "objective", "pivots",
+                           "converged", "xfull", "basis", "trace", "ntrace")}
+    for k in range(240):
+        d = 1 + k % Dx
+        m = 2 + (k * 5) % (Mx - 1)
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.2, seed=11000 + k))
+        lam = float(rng.choice([0.0, 0.01, 0.1, 1.0, 5.0]))
+        rule = "bland" if k % 6 == 0 else "dantzig_with_bland_fallback"
+        mp = int(rng.integers(1, 12)) if k % 9 == 0 else None
+        spec = ProblemSpec(data, lam)
+        cfg = SimplexConfig(max_pivots=mp, pivot_rule=rule)
+        sol = simplex_minimize(formulate(spec), cfg)
+        res = solve_lp(spec, cfg)
+        X = np.zeros((Mx, Dx)); X[:m, :d] = data.x
+        Y = np.zeros(Mx); Y[:m] = data.y
+        xf = np.full(Nx, np.nan); xf[: 2 * d + 2 * m] = sol.x
+        bs = np.full(Mx, -1); bs[:m] = sol.basis
+        tr = np.full(Tx, np.nan); nt = min(Tx, len(sol.objective_trace)); tr[:nt] = sol.objective_trace[:nt]
+        B = np.zeros(Dx); B[:d] = res.beta.beta
+        for key, v in (("x", X), ("y", Y), ("lam", lam), ("m", m), ("d", d), ("rule", int(rule == "bland")),
+                       ("max_pivots", 0 if mp is None else mp), ("beta", B), ("objective", res.objective),
+                       ("pivots", sol.pivots), ("converged", sol.converged), ("xfull", xf), ("basis", bs),
+                       ("trace", tr), ("ntrace", nt)):
+            rec[key].append(v)
+    out = {k: np.array(v) for k, v in rec.items()}
+    dumps = []
+    with tempfile.TemporaryDirectory() as tmp:
+        for k in (0, 5):
+            data, _ = generate(GenSpec(m=5 + k, d=2 + k % 3, seed=12000 + k))
+            path = os.path.join(tmp, "lp.txt")
+            dump_lp(formulate(ProblemSpec(data, 0.25)), path)
+            dumps.append(open(path).read())
+            out[f"dump{k}_x"], out[f"dump{k}_y"] = data.x.copy(), data.y.copy()
+    out["dump_text"] = np.array(dumps)
+    np.savez_compressed(os.path.join(GOLDEN, "lp.npz"), **out)
+    print("wrote lp.npz", int(out["converged"].sum()), "converged of", len(out["lam"]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count())
@@ -529,7 +584,7 @@ def main():
     with Pool(a.procs) as pool:
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
-                         ("cli", gen_cli), ("curve", gen_curve)):
+                         ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp)):
             if only is None or name in only:
                 fn(pool)
 

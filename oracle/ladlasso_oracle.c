@@ -228,6 +228,126 @@ int orc_is_axiswise_minimum(const double *x, const double *y, int m, int d, doub
 }
 
 /* ------------------------------------------------------------------ */
+/* LP recasting + dense tableau simplex (lp.py:82-215)                  */
+/* ------------------------------------------------------------------ */
+
+/* c - cb @ T with cb = 1: OpenBLAS dgemv_n row blocks of 4, pair + odd tail;
+ * columns j >= n & -4 use the scalar tail loop (sequential).  Measured with
+ * cancellation probes against numpy 2.3.5 / OpenBLAS 0.3.30. */
+static double lp_colsum(const double *T, int ld, int m, int j, int n)
+{
+    double y = 0.0;
+    if (j >= (n & -4)) {
+        for (int i = 0; i < m; ++i) y += T[i * ld + j];
+        return y;
+    }
+    int nb = m & -4;
+    for (int k = 0; k < nb; k += 4) y += ((T[k * ld + j] + T[(k + 1) * ld + j]) + T[(k + 2) * ld + j]) + T[(k + 3) * ld + j];
+    if (m - nb >= 2) y += T[nb * ld + j] + T[(nb + 1) * ld + j];
+    if ((m - nb) & 1) y += T[(m - 1) * ld + j];
+    return y;
+}
+
+/* cb @ T[:, j] (strided) with cb = 1: OpenBLAS ddot for non-unit increments */
+static double lp_strided_sum(const double *T, int ld, int m, int j)
+{
+    double t1 = 0.0, t2 = 0.0;
+    int i = 0, n1 = m & -4;
+    for (; i < n1; i += 4) {
+        t1 += T[i * ld + j] + T[(i + 2) * ld + j];
+        t2 += T[(i + 1) * ld + j] + T[(i + 3) * ld + j];
+    }
+    for (; i < m; ++i) t1 += T[i * ld + j];
+    return t1 + t2;
+}
+
+/* lp.simplex_minimize + simplex_solve.  Returns 0 ok, 1 unbounded, 3 objective mismatch (both
+ * SimplexError in the reference), -1 bad shape.
+ * x_full (2d+2m) and basis_out (m) may be NULL. */
+int orc_lp_solve(const double *x, const double *y, int m, int d, double lam, int max_pivots, int bland_rule,
+                 double tol, double *beta, double *objective, int *pivots_out, int *converged_out, double *x_full,
+                 int *basis_out)
+{
+    if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
+    const int n = 2 * d + 2 * m, ld = n + 1;
+    double *T = (double *)malloc(sizeof(double) * (size_t)(m + 1) * ld);
+    int basis[ORC_MAX_M];
+    for (int i = 0; i < m; ++i) {
+        double s = y[i] >= 0 ? 1.0 : -1.0;
+        basis[i] = y[i] >= 0 ? 2 * d + i : 2 * d + m + i;
+        for (int j = 0; j < n; ++j) {
+            double a;
+            if (j < d) a = x[i * d + j];
+            else if (j < 2 * d) a = -x[i * d + (j - d)];
+            else if (j < 2 * d + m) a = (j - 2 * d == i) ? 1.0 : 0.0;
+            else a = (j - 2 * d - m == i) ? -1.0 : 0.0;
+            T[i * ld + j] = s * a;
+        }
+        T[i * ld + n] = s * y[i];
+    }
+    for (int j = 0; j < n; ++j) T[m * ld + j] = (j < 2 * d ? lam : 1.0) - lp_colsum(T, ld, m, j, n);
+    T[m * ld + n] = -lp_strided_sum(T, ld, m, n);
+    int maxp = max_pivots > 0 ? max_pivots : 50 * n;
+    int bland = bland_rule, streak = 0, pivots = 0, converged = 0, unbounded = 0;
+    double cv[ORC_MAX_M + 1];
+    while (pivots < maxp) {
+        int col = -1;
+        if (bland) {
+            for (int j = 0; j < n; ++j)
+                if (T[m * ld + j] < -tol) { col = j; break; }
+            if (col < 0) { converged = 1; break; }
+        } else {
+            col = 0;
+            for (int j = 1; j < n; ++j)
+                if (T[m * ld + j] < T[m * ld + col]) col = j;
+            if (T[m * ld + col] >= -tol) { converged = 1; break; }
+        }
+        double ratios[ORC_MAX_M];
+        int any = 0;
+        double best = INFINITY;
+        for (int i = 0; i < m; ++i) {
+            double pc = T[i * ld + col];
+            ratios[i] = pc > tol ? T[i * ld + n] / pc : INFINITY;
+            if (pc > tol) any = 1;
+            if (ratios[i] < best) best = ratios[i];
+        }
+        if (!any) { unbounded = 1; break; }
+        int row = -1;
+        double lim = best + 1e-12 * (1.0 + fabs(best));
+        for (int i = 0; i < m; ++i)
+            if (ratios[i] <= lim && (row < 0 || basis[i] < basis[row])) row = i;
+        double piv = T[row * ld + col];
+        for (int j = 0; j <= n; ++j) T[row * ld + j] /= piv;
+        for (int i = 0; i <= m; ++i) cv[i] = i == row ? 0.0 : T[i * ld + col];
+        for (int i = 0; i <= m; ++i) {
+            if (i == row) continue;
+            for (int j = 0; j <= n; ++j) T[i * ld + j] -= cv[i] * T[row * ld + j];
+        }
+        for (int j = 0; j <= n; ++j) T[row * ld + j] -= 0.0 * T[row * ld + j];
+        for (int i = 0; i <= m; ++i) T[i * ld + col] = 0.0;
+        T[row * ld + col] = 1.0;
+        basis[row] = col;
+        ++pivots;
+        streak = best <= tol ? streak + 1 : 0;
+        if (!bland && streak >= n) bland = 1;
+    }
+    double xs[2 * ORC_MAX_D + 2 * ORC_MAX_M];
+    for (int j = 0; j < n; ++j) xs[j] = 0.0;
+    for (int i = 0; i < m; ++i) xs[basis[i]] = T[i * ld + n];
+    free(T);
+    for (int j = 0; j < d; ++j) beta[j] = xs[j] - xs[d + j];
+    *objective = orc_objective(x, y, m, d, lam, beta);
+    double cx = 0.0;
+    for (int j = 0; j < n; ++j) cx = fma(j < 2 * d ? lam : 1.0, xs[j], cx);
+    int mismatch = converged && fabs(*objective - cx) > 1e-9 * fmax(1.0, fabs(*objective));
+    *pivots_out = pivots;
+    *converged_out = converged;
+    if (x_full) memcpy(x_full, xs, sizeof(double) * n);
+    if (basis_out) memcpy(basis_out, basis, sizeof(int) * m);
+    return unbounded ? 1 : (mismatch ? 3 : 0);
+}
+
+/* ------------------------------------------------------------------ */
 /* PCG32 (rng.py:25-46)                                                 */
 /* ------------------------------------------------------------------ */
 

@@ -83,6 +83,9 @@ def lib():
         L.orc_solve_locus_batch_f32.restype = C.c_int
         L.orc_solve_locus_batch_f32.argtypes = [fp, fp, fp, C.c_longlong, C.c_int, C.c_int, C.c_double,
                                                 C.POINTER(LocusParams), C.c_int, dp, dp, ip, ip, ip, ip, lp, lp]
+        L.orc_lp_solve.restype = C.c_int
+        L.orc_lp_solve.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, dp, dp, ip,
+                                   ip, dp, ip]
         L.orc_is_axiswise_minimum.restype = C.c_int
         L.orc_is_axiswise_minimum.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp, C.c_int, C.c_double]
         L.orc_pcg32_sequence.restype = None
@@ -202,6 +205,36 @@ def is_axiswise_minimum(x, y, lam_eff, beta, skip=None, tol=1e-9) -> bool:
     if rc < 0:
         raise ValueError("problem shape outside oracle limits")
     return bool(rc)
+
+
+@dataclass
+class LpResult:
+    beta: np.ndarray
+    objective: float
+    pivots: int
+    converged: bool
+    status: int          # 0 ok, 1 unbounded, 3 objective mismatch
+    x: np.ndarray
+    basis: np.ndarray
+
+
+def lp_solve(x, y, lam_eff, max_pivots=None, pivot_rule="dantzig_with_bland_fallback", tol=1e-9) -> LpResult:
+    """lp.solve_lp restated (lp.py:106-215)."""
+    x, px = _d(x)
+    y, py = _d(y)
+    m, d = x.shape
+    beta = np.empty(d)
+    xf = np.empty(2 * d + 2 * m)
+    bs = np.empty(m, np.int32)
+    obj = C.c_double()
+    pv, cv = C.c_int(), C.c_int()
+    rc = lib().orc_lp_solve(px, py, m, d, lam_eff, 0 if max_pivots is None else int(max_pivots),
+                            1 if pivot_rule == "bland" else 0, tol, beta.ctypes.data_as(C.POINTER(C.c_double)),
+                            C.byref(obj), C.byref(pv), C.byref(cv), xf.ctypes.data_as(C.POINTER(C.c_double)),
+                            bs.ctypes.data_as(C.POINTER(C.c_int)))
+    if rc < 0:
+        raise ValueError("problem shape outside oracle limits")
+    return LpResult(beta, obj.value, pv.value, bool(cv.value), rc, xf, bs)
 
 
 def pcg32_sequence(seed, n, stream=54):

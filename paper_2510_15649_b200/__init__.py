@@ -8,11 +8,12 @@ CUDA kernels behind the C ABI in include/ladlasso_b200.h, batched over
 
 from .config import Bracket, CcdConfig, LocusConfig
 from .errors import (DegenerateInputError, DeviceError, DimensionMismatchError, InvalidInputError,
-                     ProblemTooLargeError, UnboundedDirectionError)
+                     ProblemTooLargeError, SimplexError, UnboundedDirectionError)
 from .solver import (BatchedSolveResult, Coefficients, Dataset, ProblemSpec, SolveResult, axiswise_minimum_batched,
                      ccd_descend, ccd_descend_batched, evaluate_objective, evaluate_objective_batched,
                      is_axiswise_minimum, solve_brute, solve_brute_batched, solve_ccd, solve_locus,
                      solve_locus_batched)
+from .lp import SimplexConfig, SimplexSolution, solve_lp, solve_lp_batched
 from .curve import (LocusPoint, axes_by_influence, default_bracket, default_outer_axis, locus_value,
                     perturb_restart, sample_locus, sample_locus_batched)
 
@@ -25,4 +26,5 @@ __all__ = [
     "evaluate_objective_batched", "solve_brute", "solve_brute_batched", "solve_ccd", "solve_locus",
     "solve_locus_batched", "axiswise_minimum_batched", "is_axiswise_minimum", "LocusPoint", "axes_by_influence",
     "default_bracket", "default_outer_axis", "locus_value", "perturb_restart", "sample_locus", "sample_locus_batched",
+    "SimplexConfig", "SimplexSolution", "SimplexError", "solve_lp", "solve_lp_batched",
 ]

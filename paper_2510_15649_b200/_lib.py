@@ -31,6 +31,7 @@ SYMBOLS = (
     "lad_ccd_descend_f32",
     "lad_fp32_peak_tflops",
     "lad_axiswise_minimum_f64",
+    "lad_lp_solve_f64",
 )
 
 LAD_OK = 0
@@ -126,6 +127,8 @@ def load(build_if_missing: bool = False):
     L.lad_brute_solve_f64.argtypes = [vp, vp, vp, i64, i32, i32, i32, i64, dbl, vp, vp, vp, vp]
     L.lad_objective_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, dbl, vp, vp]
     L.lad_axiswise_minimum_f64.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, dbl, dbl, vp, vp]
+    L.lad_lp_solve_f64.argtypes = [vp, vp, vp, i64, i32, i32, i32, i32, dbl, dbl, vp, vp, vp, vp, vp, vp, vp, vp,
+                                   i32, vp]
     L.lad_generate_f64.argtypes = [i32, C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp, vp]
     L.lad_subsets_f64.argtypes = [vp, vp, i32, i32, i32, i64, i64, vp, vp, vp]
     L.lad_kernel_launches.restype = C.c_longlong

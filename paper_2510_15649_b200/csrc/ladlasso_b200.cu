@@ -16,6 +16,7 @@
 #include "../../include/ladlasso_b200.h"
 #include "lad_brute.cuh"
 #include "lad_cert.cuh"
+#include "lad_lp.cuh"
 #include "lad_gen.cuh"
 #include "lad_locus.cuh"
 #include "lad_locus_warp.cuh"
@@ -574,5 +575,30 @@ extern "C" int lad_axiswise_minimum_f64(const double *X, const double *Y, const 
     lad::axiswise_minimum_kernel<32, 8><<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(A); ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(LAD_E_CUDA, "certificate kernel: %s", cudaGetErrorString(e));
+    return LAD_OK;
+}
+
+extern "C" int lad_lp_solve_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
+                                int32_t max_pivots, int32_t pivot_rule, double feasibility_tolerance,
+                                double lambda_floor, double *beta, double *objective, int32_t *pivots,
+                                uint8_t *converged, uint8_t *status, double *x_full, int32_t *basis, double *trace,
+                                int32_t trace_cap, void *stream)
+{
+    if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1");
+    if (n > lad::LP_MMAX || p > lad::LP_DMAX) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+    if (max_pivots < 0) return fail(LAD_E_INVALID, "max_pivots must be at least 1 (0 = default 50 * columns)");
+    if (pivot_rule != LAD_PIVOT_DANTZIG_BLAND && pivot_rule != LAD_PIVOT_BLAND)
+        return fail(LAD_E_INVALID, "unknown pivot rule %d", pivot_rule);
+    if (!(lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
+    if (!beta || !objective || !pivots || !converged || !status) return fail(LAD_E_INVALID, "output pointers must be non-null");
+    if (B == 0) return LAD_OK;
+    const size_t smem = lad::lp_smem_bytes();
+    CK(cudaFuncSetAttribute(lad::lp_simplex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    lad::LpArgs A{X, Y, lam, B, n, p, max_pivots, pivot_rule == LAD_PIVOT_BLAND, feasibility_tolerance, lambda_floor,
+                  beta, objective, x_full, pivots, basis, converged, status, trace, trace ? trace_cap : 0};
+    const unsigned grid = (unsigned)((B + lad::LP_WARPS - 1) / lad::LP_WARPS);
+    lad::lp_simplex_kernel<<<grid, 32 * lad::LP_WARPS, smem, (cudaStream_t)stream>>>(A); ++g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(LAD_E_CUDA, "simplex kernel: %s", cudaGetErrorString(e));
     return LAD_OK;
 }

@@ -212,7 +212,7 @@ def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=N
         Xt, yt, lt = _validate_device(X, y, lam, None, f32)
         dev = Xt.device
     B, n, p = Xt.shape
-    st = torch.as_tensor(np.asarray(start, dtype=np.float64) if not _is_torch(start) else start,
+    st = torch.as_tensor(np.array(start, dtype=np.float64) if not _is_torch(start) else start,
                          dtype=torch.float64, device=dev).reshape(-1, p).expand(B, p).contiguous()
     if frozen is None and getattr(cfg, "frozen_axis", None) is not None:
         frozen = cfg.frozen_axis

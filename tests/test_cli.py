@@ -168,13 +168,9 @@ def test_check_task_picker_matches_reference():
     assert got == _fixture()["check_tasks_seed0"]
 
 
-def test_out_of_scope_solver_is_an_input_error(tmp_path, capsys):
-    p = tmp_path / "d.csv"
-    write_dataset_csv(generate(GenSpec(m=5, d=2))[0], p)
-    assert cli.main(["solve", str(p), "--lambda", "0.1", "--solver", "lp"]) == 1
-    assert "outside this framework" in capsys.readouterr().err
-    assert cli.main(["solve", str(p), "--lambda", "0.1", "--dump-lp", str(tmp_path / "lp.txt")]) == 1
-    assert cli.main(["bench", "--solvers", "lp", "--out", str(tmp_path / "b.csv")]) == 1
+def test_unknown_bench_solver_is_an_input_error(tmp_path, capsys):
+    assert cli.main(["bench", "--solvers", "simplex2", "--out", str(tmp_path / "b.csv")]) == 1
+    assert "unknown solver" in capsys.readouterr().err
 
 
 def test_solve_missing_file_exit_1(tmp_path, capsys):
@@ -221,13 +217,23 @@ def test_check_matches_reference_transcript(tmp_path, capsys):
         code = cli.main(["check"] + case["argv"] + ["--out", str(out)])
         stdout = capsys.readouterr().out
         assert code == case["code"], case["argv"]
-        ref_lines = [ln for ln in case["stdout"].strip().split("\n") if not ln.startswith("lp:")]
-        assert stdout.strip().split("\n") == ref_lines
+        assert stdout.strip().split("\n") == case["stdout"].strip().split("\n")
         rh, rrows = _table(case["csv"])
         mh, mrows = _table(out.read_text())
-        assert mh == [c for c in rh if not c.endswith("_lp")]
+        assert mh == rh
         cols = [c for c in mh if not c.startswith("time_")]
         assert [[r[c] for c in cols] for r in mrows] == [[r[c] for c in cols] for r in rrows]
+
+
+@pytest.mark.gpu
+def test_solve_dump_lp_matches_reference_bytes(tmp_path, capsys):
+    fx = _fixture()
+    path = tmp_path / "s.csv"
+    path.write_text(fx["solve_csv"])
+    lp_path = tmp_path / "s.lp"
+    assert cli.main(["solve", str(path), "--lambda", "0.3", "--solver", "lp", "--dump-lp", str(lp_path)]) == 0
+    capsys.readouterr()
+    assert lp_path.read_text() == fx["dump_lp"]
 
 
 @pytest.mark.gpu
