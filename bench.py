@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4],
                     help="BASELINE config (2 = the metric's n=30/p=5 lambda path, the default)")
     ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
+    ap.add_argument("--solver", choices=["locus", "lp", "brute"], default="locus",
+                    help="locus (the metric); lp = the simplex on config-2 problems; brute = the check on config 1")
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
                     help="f32: the fp32 mode (binary32 data and descents; config 4 runs in both)")
     return ap.parse_args()
@@ -253,6 +255,160 @@ class Workload:
         return X[:m].cpu().numpy(), Y[:m].cpu().numpy(), L[:m].cpu().numpy()
 
 
+def lp_flops(pivots, m, d):
+    """Algorithmic FP64 flops of the dense tableau simplex: per pivot (n+1) divisions for the pivot
+    row + 2 (mul, sub) per entry of the other m rows; setup m*n products + (m+1)*n sums."""
+    n = 2 * d + 2 * m
+    return pivots * ((n + 1) + 2 * m * (n + 1)) + 2 * (m + 1) * n
+
+
+def brute_flops(vertices, m, d):
+    """Per nonsingular vertex: Gaussian elimination (2/3 d^3 + 2 d^2) and the objective (2md + 2m + 2d)."""
+    return vertices * (2.0 / 3.0 * d ** 3 + 2 * d * d + 2 * m * d + 2 * m + 2 * d)
+
+
+def run_aux(a, world, rank, local):
+    """--solver lp | brute: the widened rows (the check of §8a a17), same protocol."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2510_15649_b200 as lad
+    from paper_2510_15649_b200 import _lib, generate as G
+    from paper_2510_15649_b200.solver import fp64_peak_tflops
+
+    if a.solver == "lp":
+        config, B = 2, 1 << 16
+        n, p = G.CONFIG_SHAPES[2]
+        desc = f"simplex (lp.solve_lp) on config-2 problems: {B} (dataset, lambda) pairs per step, n=30, p=5"
+        steps_inputs = []
+        for s_ in range(a.warmup + a.steps):
+            X, Y, _ = G.generate(2, B // 16, seed=SEED, first=((s_ * world + rank) * (B // 16)) % TOTAL_DATASETS,
+                                 device=dev)
+            idx = torch.arange(B // 16, device=dev).repeat_interleave(16)
+            lam = torch.tensor(LAMBDA_GRID, device=dev, dtype=torch.float64).repeat(B // 16)
+            steps_inputs.append((X[idx].contiguous(), Y[idx].contiguous(), lam))
+
+        def solve(k):
+            X, Y, L = steps_inputs[k]
+            return lad.solve_lp_batched(X, Y, L)
+
+        def flops(r):
+            return lp_flops(float(r.pivots.double().sum()), n, p)
+    else:
+        config, B = 1, 1 << 20
+        n, p = G.CONFIG_SHAPES[1]
+        desc = f"brute-force vertex check (brute.solve_brute) on config 1: B={B}, n=10, p=2, C(12,2)=66 vertices"
+        steps_inputs = [G.generate(1, B, seed=SEED - 2 + 1, first=(s_ * world + rank) * B, device=dev)
+                        for s_ in range(a.warmup + a.steps)]
+
+        def solve(k):
+            X, Y, L = steps_inputs[k]
+            return lad.solve_brute_batched(X, Y, L)
+
+        def flops(r):
+            return brute_flops(float(r[2].double().sum()), n, p)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    peak = fp64_peak_tflops()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for k in range(a.warmup):
+        solve(k)
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    results = []
+    launches0 = _lib.kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(a.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            results.append(solve(a.warmup + k))
+            evs[k][1].record(stream)
+        barrier()
+    gpu_launches = _lib.kernel_launches() - launches0
+    clocks = clk.summary()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    elapsed = sum(step_ms) / 1e3
+    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value = world * a.steps * B / float(t.item())
+    fl = sum(flops(r) for r in results)
+    achieved = fl / elapsed / 1e12
+    # e2e through the public API with host (pinned) inputs and host outputs
+    hosts = []
+    for k in range(min(a.steps, 3)):
+        hx, hy, hl = (torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v) for v in steps_inputs[a.warmup + k])
+        hosts.append((hx.numpy(), hy.numpy(), hl.numpy()))
+    run_host = (lambda h: lad.solve_lp_batched(*h)) if a.solver == "lp" else (lambda h: lad.solve_brute_batched(*h))
+    run_host(tuple(v[:256] for v in hosts[0]))
+    barrier()
+    t0 = time.perf_counter()
+    for h in hosts:
+        run_host(h)
+    barrier()
+    e2e_value = world * len(hosts) * B / (time.perf_counter() - t0)
+    h2d = sum(v.nbytes for v in hosts[0])
+    d2h = B * (p * 8 + 8 + 4 + 1 + 1) if a.solver == "lp" else B * (p * 8 + 8 + 8)
+    cpu = parity = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        from oracle import oracle as O
+
+        O.build()
+        Xh, Yh, Lh = (v.cpu().numpy() for v in steps_inputs[a.warmup])
+        g = results[0]
+        t0 = time.perf_counter()
+        nsol = exact = 0
+        while nsol < B and time.perf_counter() - t0 < 10.0:  # single-thread oracle, ~10 s sample
+            lam_eff = max(float(Lh[nsol]), 1e-9)
+            if a.solver == "lp":
+                o = O.lp_solve(Xh[nsol], Yh[nsol], lam_eff)
+                gb, go = g.beta[nsol].cpu().numpy(), float(g.objective[nsol])
+                ok = np.array_equal(gb, o.beta) and go == o.objective and int(g.pivots[nsol]) == o.pivots
+            else:
+                ob, oo, ov = O.solve_brute(Xh[nsol], Yh[nsol], lam_eff)
+                ok = np.array_equal(g[0][nsol].cpu().numpy(), ob) and float(g[1][nsol]) == oo
+            exact += int(ok)
+            nsol += 1
+        dt = time.perf_counter() - t0
+        what = "lp.solve_lp (oracle orc_lp_solve)" if a.solver == "lp" else "brute.solve_brute (oracle orc_solve_brute)"
+        cpu = {"value": nsol / dt, "unit": "solves/s", "cores": 1, "kind": "port",
+               "sample": f"first {nsol} problems of the first timed step, {what}, 1 thread, {dt:.1f} s "
+                         "(includes the GPU-vs-oracle comparison)"}
+        parity = {"sample": nsol, "bit_exact": exact}
+    if rank == 0:
+        metric = ("LP (dense simplex) solves/sec (n=30,p=5 fp64)" if a.solver == "lp"
+                  else "brute-force vertex checks/sec (config 1: n=10,p=2 fp64)")
+        print(json.dumps({
+            "metric": metric, "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": float(t.item()) * 1e3 / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device Philox generator with the BASELINE config distributions)",
+            "config": {"workload": f"{a.solver}_config{config}", "description": desc, "n": n, "p": p,
+                       "solves_per_step_per_gpu": B, "parallelism": f"shard{world} (independent problems)",
+                       "l2": "flushed between steps (256 MiB memset)"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "flops_model": "bench.lp_flops" if a.solver == "lp" else "bench.brute_flops"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": len(hosts)},
+            "gpu_launches": gpu_launches, "clocks": clocks, "parity_sample": parity, "step_ms": step_ms}),
+            flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -260,6 +416,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         return run_reference(a, rank, world)
+    if a.solver != "locus":
+        return run_aux(a, world, rank, local)
 
     import torch
     import torch.distributed as dist
