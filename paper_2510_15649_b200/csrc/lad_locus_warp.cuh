@@ -64,6 +64,7 @@ struct WarpShared {
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
     int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
+    int cand2[PMAX];     // per axis: the one before (the median often alternates between two elements)
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
 };
@@ -390,15 +391,26 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     T t_new;
     bool hit = false;
     if (cacheable) {
-        const int m = W->cand[j];
-        const T lm = shfl_t(loc, m);
-        const bool below = (loc < lm) | ((loc == lm) & (lane < m));
         const unsigned q = W->wq[j][lane];
-        const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
-        const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
         const unsigned hq = W->halfq[j];
-        hit = (qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q);  // exact integers: warp-uniform
-        t_new = lm;
+        const int m1 = W->cand[j];
+        // is element m the median?  (exact integer sums: the answer is warp-uniform)
+        auto test = [&](int m, T &lm) {
+            lm = shfl_t(loc, m);
+            const bool below = (loc < lm) | ((loc == lm) & (lane < m));
+            const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
+            const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
+            return (qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q);
+        };
+        hit = test(m1, t_new);
+        if (!hit) {
+            const int m2 = W->cand2[j];
+            if (m2 != m1 && test(m2, t_new)) {
+                hit = true;
+                W->cand2[j] = m1;  // identical value from every lane
+                W->cand[j] = m2;
+            }
+        }
     }
     if (!hit) {
     // stable order by (location, index).  The order is unique, so if this
@@ -460,7 +472,12 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     const T tk = shfl_t(key, ks);
     const T tk1 = shfl_t(key, ks + 1 < 32 ? ks + 1 : 31);
     t_new = tie ? dmul(T(0.5), dadd(tk, tk1)) : tk;
-    if (cacheable) W->cand[j] = __shfl_sync(FULLMASK, idx, ks);  // identical value from every lane
+    if (cacheable) {  // identical values from every lane
+        const int mnew = __shfl_sync(FULLMASK, idx, ks);
+        W->cand2[j] = W->cand[j];
+        __syncwarp();
+        W->cand[j] = mnew;
+    }
     }
     if (fabs(dsub(t_new, bj)) <= dmul(T(1e-14), dadd(T(1), fabs(bj)))) return;  // ccd.py:172
     T constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
@@ -648,6 +665,7 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, 4) locus_warp_kernel(Loc
     uint32_t perm_valid = 0;
     Ctl<PMAX> &C = W->C;
     if (lane < PMAX) W->cand[lane] = 0;
+    if (lane < PMAX) W->cand2[lane] = 1;
     if (lane == 0) C.pc = PC_FETCH;
     __syncwarp();
     for (;;) {
