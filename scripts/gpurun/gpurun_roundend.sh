@@ -8,4 +8,4 @@ python bench.py --config 4 --dtype f32 --steps 3 --warmup 3 > gpurun_out/bench_c
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --block 2048 --no-cpu > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"
 python bench.py --solver lp --steps 3 --warmup 2 > gpurun_out/bench_lp.json 2> gpurun_out/bench_lp.err; echo "lp rc=$?"
 python bench.py --solver brute --steps 3 --warmup 2 > gpurun_out/bench_brute.json 2> gpurun_out/bench_brute.err; echo "brute rc=$?"
-bash gpurun_fullprof.sh
+bash scripts/gpurun/gpurun_fullprof.sh
