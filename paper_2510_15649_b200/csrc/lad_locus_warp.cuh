@@ -39,19 +39,6 @@ constexpr int WARPS_PER_BLOCK = 7;
 template <int PMAX, typename T>
 constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5;
 
-__device__ __forceinline__ bool div_operand_safe(double v)
-{
-    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
-    return hi - (573u << 20) < ((1474u - 573u) << 20);  // 2^-450 <= |v| < 2^451
-}
-__device__ __forceinline__ bool div_operand_safe(float v)
-{
-    const unsigned b = (unsigned)__float_as_int(v) & 0x7fffffffu;
-    return b - (77u << 23) < ((178u - 77u) << 23);  // 2^-50 <= |v| < 2^51
-}
-__device__ __forceinline__ double rcp_rn(double v) { return __drcp_rn(v); }
-__device__ __forceinline__ float rcp_rn(float v) { return __frcp_rn(v); }
-
 template <int PMAX, typename T>
 struct WarpShared {
     using T2 = typename vec2_of<T>::type;
@@ -542,13 +529,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
         const T rr = row ? r : T(1), xx = row ? xij : T(1);
         T q;
         if constexpr (fast_div_v<PMAX, T>) {
-            const T y = yrow[j];  // 1 on pad lanes
-            q = dmul(rr, y);
-            T e = dfma(-q, xx, rr);
-            q = dfma(e, y, q);
-            e = dfma(-q, xx, rr);
-            q = dfma(e, y, q);
-            if (!div_operand_safe(rr)) q = (rr == T(0)) ? dmul(rr, y) : ddiv(rr, xx);  // rare, divergent
+            q = div_by_rcp(rr, xx, yrow[j]);  // y = 1 on pad lanes
         } else {
             q = ddiv(rr, xx);
         }

@@ -22,6 +22,37 @@ __device__ __forceinline__ float dmul(float a, float b) { return __fmul_rn(a, b)
 __device__ __forceinline__ float ddiv(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float dfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
+// Division by a precomputed reciprocal y = RN(1/b): q = RN(a*y) and two
+// corrections q += RN(a - q*b)*y.  The first makes q faithful, the second then
+// rounds correctly (Markstein), so the result equals a / b in round-to-nearest
+// whenever nothing under- or overflows: |a|, |b| within 2^+-450 (binary64) or
+// 2^+-50 (binary32); callers route other b to the generic division and the
+// rare other a are handled here.
+__device__ __forceinline__ bool div_operand_safe(double v)
+{
+    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
+    return hi - (573u << 20) < ((1474u - 573u) << 20);  // 2^-450 <= |v| < 2^451
+}
+__device__ __forceinline__ bool div_operand_safe(float v)
+{
+    const unsigned b = (unsigned)__float_as_int(v) & 0x7fffffffu;
+    return b - (77u << 23) < ((178u - 77u) << 23);  // 2^-50 <= |v| < 2^51
+}
+__device__ __forceinline__ double rcp_rn(double v) { return __drcp_rn(v); }
+__device__ __forceinline__ float rcp_rn(float v) { return __frcp_rn(v); }
+
+template <typename T>
+__device__ __forceinline__ T div_by_rcp(T a, T b, T y)
+{
+    T q = dmul(a, y);
+    T e = dfma(-q, b, a);
+    q = dfma(e, y, q);
+    e = dfma(-q, b, a);
+    q = dfma(e, y, q);
+    if (!div_operand_safe(a)) q = (a == T(0)) ? dmul(a, y) : ddiv(a, b);  // rare, divergent
+    return q;
+}
+
 template <typename T>
 __device__ __forceinline__ T inf_of();
 template <>
