@@ -1108,9 +1108,12 @@ __global__ void __launch_bounds__(32) locus_kernel(LocusArgs A)
         __syncwarp();
         if (!alive || need_ctl) continue;
         // ---- one coordinate step on axis j
-        if (EXACT && !((sparse >> j) & 1u)) {
-            step_dense<NMAX, PMAX>(r, b, Xs, Ls, lane, j, lam, f_cur, sum_abs_b);
-        } else {
+        bool dense_step = false;
+        if constexpr (EXACT) {
+            dense_step = !((sparse >> j) & 1u);
+            if (dense_step) step_dense<NMAX, PMAX>(r, b, Xs, Ls, lane, j, lam, f_cur, sum_abs_b);
+        }
+        if (!dense_step) {
             // rare path (zero entries in column j, or runtime-shape kernel): work on
             // local copies so the register arrays never have their address taken
             double rl[NMAX], bl[PMAX];

@@ -7,8 +7,9 @@
 // switch to Bland's rule after a degenerate streak of n pivots, ratio test
 // with 1e-12 relative ties broken by the smallest basic variable index.
 //
-// One warp per problem, tableau (m+1) x (n+1) in shared memory, lanes over
-// columns for row operations and over rows for the ratio test.  Bit-exact
+// One warp per problem, tableau (m+1) x (n+1) in shared memory (sized per
+// launch), lanes over columns for row operations and over rows (two per lane,
+// m <= 46) for the ratio test.  Bit-exact
 // with the reference: the pivot update is numpy's elementwise
 // `row /= piv; T -= outer(col, row)` (two roundings per entry), and the
 // initial reduced-cost row c - cb @ T and objective cell -(cb @ T[:, n])
@@ -23,8 +24,8 @@
 
 namespace lad {
 
-constexpr int LP_MMAX = 32, LP_DMAX = 8;
-constexpr int LP_NMAX = 2 * LP_DMAX + 2 * LP_MMAX;  // 80 columns
+constexpr int LP_MMAX = 46, LP_DMAX = 8;
+constexpr int LP_NMAX = 2 * LP_DMAX + 2 * LP_MMAX;  // 108 columns
 constexpr int LP_WARPS = 4;
 
 struct LpArgs {
@@ -39,7 +40,11 @@ struct LpArgs {
     uint8_t *converged, *status;       // 0 ok, 1 unbounded, 2 invalid input, 3 objective mismatch
     double *trace;                     // (B, trace_cap) objective after 0, 1, ... pivots; may be null
     int trace_cap;
+    int warp_doubles;                  // shared memory per warp: tableau (m+1)(n+1) + pivot column (m+1)
 };
+
+// shared memory per warp for an m-row, d-variable problem
+__host__ __device__ inline int lp_warp_doubles(int m, int d) { return (m + 1) * (2 * d + 2 * m + 1) + m + 1; }
 
 // c - cb @ T column sum with cb = 1 (every initial basic variable is a residual
 // part of cost 1): OpenBLAS dgemv_n folds rows in blocks of 4 ((t0+t1)+t2)+t3
@@ -84,8 +89,8 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
     const int64_t pr = (int64_t)blockIdx.x * LP_WARPS + w;
     if (pr >= A.B) return;
     const int m = A.m, d = A.d, n = 2 * d + 2 * m, ld = n + 1;
-    double *T = lp_smem + (size_t)w * ((LP_MMAX + 1) * (LP_NMAX + 1) + LP_MMAX + 1);
-    double *cv = T + (LP_MMAX + 1) * (LP_NMAX + 1);  // pivot column copy (m+1)
+    double *T = lp_smem + (size_t)w * A.warp_doubles;
+    double *cv = T + (size_t)(m + 1) * ld;  // pivot column copy (m+1)
     const double *x = A.X + (size_t)pr * m * d, *y = A.Y + (size_t)pr * m;
     const double lraw = A.lam[pr];
     bool ok = isfinite(lraw) && lraw >= 0.0;
@@ -103,10 +108,14 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
         return;
     }
     const double lam = lraw > A.lambda_floor ? lraw : A.lambda_floor;
-    // row i of lane i: basis index and sign of y_i (lp.initial_basis, lp.py:99-103)
-    const bool row_lane = lane < m;
-    const double yi = row_lane ? y[lane] : 0.0;
-    int basis = row_lane ? (yi >= 0.0 ? 2 * d + lane : 2 * d + m + lane) : 0x7fffffff;
+    // rows lane and lane + 32 belong to this lane: their basic variables
+    // (lp.initial_basis, lp.py:99-103: rp_i where y_i >= 0, else rn_i)
+    int bas[2];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        const int i = lane + 32 * sl;
+        bas[sl] = i < m ? (y[i] >= 0.0 ? 2 * d + i : 2 * d + m + i) : 0x7fffffff;
+    }
     // tableau[:m, :n] = sign * A, tableau[:m, n] = sign * b
     for (int e = lane; e < m * ld; e += 32) {
         const int i = e / ld, j = e - i * ld;
@@ -178,21 +187,31 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
             }
         }
         // leaving row: min ratio, ties within 1e-12 relative -> smallest basic index
-        const double pc = row_lane ? T[lane * ld + col] : 0.0;
-        const bool elig = row_lane && pc > tol;
-        if (!__any_sync(0xffffffffu, elig)) {
+        double ratio[2];
+        bool elig_any = false;
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+            const int i = lane + 32 * sl;
+            const double pc = i < m ? T[i * ld + col] : 0.0;
+            const bool elig = i < m && pc > tol;
+            elig_any = elig_any || elig;
+            ratio[sl] = elig ? ddiv(T[i * ld + n], pc) : __longlong_as_double(0x7ff0000000000000LL);
+        }
+        if (!__any_sync(0xffffffffu, elig_any)) {
             unbounded = true;
             break;
         }
-        const double ratio = elig ? ddiv(T[lane * ld + n], pc) : __longlong_as_double(0x7ff0000000000000LL);
-        double best = ratio;
+        double best = fmin(ratio[0], ratio[1]);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, off));
-        const bool tie = row_lane && ratio <= dadd(best, dmul(1e-12, dadd(1.0, fabs(best))));
-        int key = tie ? basis : 0x7fffffff;
+        const double lim = dadd(best, dmul(1e-12, dadd(1.0, fabs(best))));
+        const bool tie0 = lane < m && ratio[0] <= lim, tie1 = lane + 32 < m && ratio[1] <= lim;
+        int key = min(tie0 ? bas[0] : 0x7fffffff, tie1 ? bas[1] : 0x7fffffff);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, off));
-        const int row = __ffs(__ballot_sync(0xffffffffu, tie && basis == key)) - 1;
+        const unsigned b0 = __ballot_sync(0xffffffffu, tie0 && bas[0] == key);
+        const unsigned b1 = __ballot_sync(0xffffffffu, tie1 && bas[1] == key);
+        const int row = b0 ? __ffs(b0) - 1 : 32 + __ffs(b1) - 1;
         // pivot: row /= piv; T -= outer(col_vals, row) with col_vals[row] = 0
         const double piv = T[row * ld + col];
         for (int i = lane; i <= m; i += 32) cv[i] = (i == row) ? 0.0 : T[i * ld + col];
@@ -209,7 +228,8 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
         for (int j = lane; j <= n; j += 32) T[row * ld + j] = dsub(T[row * ld + j], dmul(0.0, T[row * ld + j]));
         __syncwarp();
         for (int i = lane; i <= m; i += 32) T[i * ld + col] = (i == row) ? 1.0 : 0.0;
-        if (lane == row) basis = col;
+        if (lane == row) bas[0] = col;
+        if (lane + 32 == row) bas[1] = col;
         __syncwarp();
         ++pivots;
         if (trace && lane == 0 && pivots < A.trace_cap) trace[pivots] = -T[m * ld + n];
@@ -221,12 +241,17 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
     __syncwarp();
     for (int j = lane; j < n; j += 32) xs[j] = 0.0;
     __syncwarp();
-    if (row_lane) xs[basis] = T[lane * ld + n];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl)
+        if (lane + 32 * sl < m) xs[bas[sl]] = T[(lane + 32 * sl) * ld + n];
     __syncwarp();
     for (int j = lane; j < d; j += 32) A.beta[(size_t)pr * d + j] = dsub(xs[j], xs[d + j]);
     if (A.xfull)
         for (int j = lane; j < n; j += 32) A.xfull[(size_t)pr * n + j] = xs[j];
-    if (A.basis && row_lane) A.basis[(size_t)pr * m + lane] = basis;
+    if (A.basis)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl)
+            if (lane + 32 * sl < m) A.basis[(size_t)pr * m + lane + 32 * sl] = bas[sl];
     __syncwarp();
     if (lane == 0) {
         // evaluate_objective(beta) (model.py:151) and the consistency check of simplex_solve (lp.py:180-186)
@@ -245,6 +270,5 @@ __global__ void __launch_bounds__(32 * LP_WARPS) lp_simplex_kernel(LpArgs A)
     }
 }
 
-inline size_t lp_smem_bytes() { return (size_t)LP_WARPS * ((LP_MMAX + 1) * (LP_NMAX + 1) + LP_MMAX + 1) * sizeof(double); }
 
 }  // namespace lad

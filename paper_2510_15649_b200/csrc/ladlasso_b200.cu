@@ -119,6 +119,8 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
     if (thread_exact) v = make_thread_variant<10, 2, true>();
     else if (n <= 16 && p <= 4) v = make_thread_variant<16, 4, false>();
     else if (n <= 32 && p <= 8) v = make_thread_variant<32, 8, false>();
+    else if (n <= 46 && p <= 4) v = make_thread_variant<48, 4, false>();  // n + 1 <= 47: the modelled ddot range
+    else if (n <= 46 && p <= 8) v = make_thread_variant<48, 8, false>();
     else return false;
     return true;
 }
@@ -160,7 +162,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     if (!(prm->lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     Variant v;
     if (!pick_variant(n, p, v, f32))
-        return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : 32);
+        return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : 46);
 
     if (g_num_sms == 0) {
         int dev;
@@ -567,12 +569,12 @@ extern "C" int lad_axiswise_minimum_f64(const double *X, const double *Y, const 
                                         double lambda_floor, uint8_t *out, void *stream)
 {
     if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1");
-    if (n > 32 || p > 8) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+    if (n > 64 || p > 8) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=64, p<=8", n, p);
     if (!(tol >= 0)) return fail(LAD_E_INVALID, "tol must be >= 0");
     if (!(lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     if (B == 0) return LAD_OK;
     lad::CertArgs A{X, Y, lam, beta, skip, B, n, p, tol, lambda_floor, out};
-    lad::axiswise_minimum_kernel<32, 8><<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(A); ++g_launches;
+    lad::axiswise_minimum_kernel<64, 8><<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(A); ++g_launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(LAD_E_CUDA, "certificate kernel: %s", cudaGetErrorString(e));
     return LAD_OK;
@@ -585,17 +587,18 @@ extern "C" int lad_lp_solve_f64(const double *X, const double *Y, const double *
                                 int32_t trace_cap, void *stream)
 {
     if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1");
-    if (n > lad::LP_MMAX || p > lad::LP_DMAX) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=32, p<=8", n, p);
+    if (n > lad::LP_MMAX || p > lad::LP_DMAX) return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=46, p<=8", n, p);
     if (max_pivots < 0) return fail(LAD_E_INVALID, "max_pivots must be at least 1 (0 = default 50 * columns)");
     if (pivot_rule != LAD_PIVOT_DANTZIG_BLAND && pivot_rule != LAD_PIVOT_BLAND)
         return fail(LAD_E_INVALID, "unknown pivot rule %d", pivot_rule);
     if (!(lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     if (!beta || !objective || !pivots || !converged || !status) return fail(LAD_E_INVALID, "output pointers must be non-null");
     if (B == 0) return LAD_OK;
-    const size_t smem = lad::lp_smem_bytes();
+    const int warp_doubles = lad::lp_warp_doubles(n, p);
+    const size_t smem = (size_t)lad::LP_WARPS * warp_doubles * sizeof(double);
     CK(cudaFuncSetAttribute(lad::lp_simplex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     lad::LpArgs A{X, Y, lam, B, n, p, max_pivots, pivot_rule == LAD_PIVOT_BLAND, feasibility_tolerance, lambda_floor,
-                  beta, objective, x_full, pivots, basis, converged, status, trace, trace ? trace_cap : 0};
+                  beta, objective, x_full, pivots, basis, converged, status, trace, trace ? trace_cap : 0, warp_doubles};
     const unsigned grid = (unsigned)((B + lad::LP_WARPS - 1) / lad::LP_WARPS);
     lad::lp_simplex_kernel<<<grid, 32 * lad::LP_WARPS, smem, (cudaStream_t)stream>>>(A); ++g_launches;
     cudaError_t e = cudaGetLastError();
