@@ -399,6 +399,7 @@ def run_aux(a, world, rank, local):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "flops_model": "bench.lp_flops" if a.solver == "lp" else "bench.brute_flops"},
+            "issue_roofline": issue,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": len(hosts)},
@@ -514,12 +515,24 @@ def main():
     h2d = host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes + (hidx_np.nbytes if hidx_np is not None else 0)
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
 
-    # DRAM traffic per launch from the committed ncu --set full capture of this workload (None otherwise)
+    # DRAM traffic per launch and warp instructions per coordinate step from the committed
+    # ncu --set full capture of this workload (None otherwise)
     traffic = None
+    issue = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"config{a.config}_{a.dtype}")
         if tr:
             traffic = tr["bytes_per_solve"] * solves_per_step
+            ipc = tr.get("warp_instr_per_coord_step")
+            if ipc and clocks.get("sm_mhz"):
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                peak_issue = 4 * sms * clocks["sm_mhz"] * 1e6  # one warp instruction per SMSP per cycle
+                ach_issue = ipc * S / elapsed
+                issue = {"bound": "issue", "achieved": ach_issue / 1e9, "peak": peak_issue / 1e9,
+                         "unit": "G warp-instr/s", "frac": ach_issue / peak_issue,
+                         "warp_instr_per_coord_step": ipc,
+                         "source": "instr/step from profiles/ncu_traffic.json x live coordinate steps/s; "
+                                   "peak = 4 SMSPs x SMs x sampled SM clock"}
     except (OSError, ValueError):
         pass
     cpu = None
@@ -571,6 +584,7 @@ def main():
                          "flops_per_solve": fl / (a.steps * solves_per_step),
                          "coord_steps_per_solve": S / (a.steps * solves_per_step),
                          "descents_per_solve": D / (a.steps * solves_per_step)},
+            "issue_roofline": issue,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
