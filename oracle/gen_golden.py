@@ -573,6 +573,59 @@ def gen_lp(pool):
     print("wrote lp.npz", int(out["converged"].sum()), "converged of", len(out["lam"]))
 
 
+def gen_large(pool):
+    """Problems beyond 46 rows (block-per-problem path): ccd_descend with m up to 1000 (sparse columns
+    included) and solve_locus (both variants, work counters) with m up to 256."""
+    _ref()
+    from ladlasso.datagen import GenSpec, generate
+
+    rng = np.random.default_rng(9090)
+    cp = []
+    for i in range(48):
+        m = int((47, 48, 64, 100, 127, 129, 200, 333, 500, 1000)[i % 10])
+        d = 1 + i % 8
+        x = rng.standard_normal((m, d)) * rng.choice([1.0, 3.0])
+        if i % 4 == 0:
+            x[rng.random((m, d)) < 0.1] = 0.0
+        y = x @ np.where(rng.random(d) < 0.5, rng.uniform(1, 3, d), 0.0) + rng.laplace(0, 0.5, m)
+        cp.append(dict(x=x, y=y, lam=float(rng.choice([0.01, 0.1, 1.0])), start=rng.standard_normal(d) * (i % 2),
+                       frozen=None if i % 3 else int(rng.integers(0, d)), tol=1e-10, sweeps=500))
+    cres = pool.map(_task, [("ccd", q) for q in cp], chunksize=1)
+    lp_ = []
+    for i in range(24):
+        m = int((47, 60, 100, 150, 256, 64)[i % 6])
+        d = (2, 3, 5, 8)[i % 4]
+        data, _ = generate(GenSpec(m=m, d=d, noise_sigma=1.0, outlier_fraction=0.1, seed=21000 + i))
+        lp_.append(dict(x=data.x, y=data.y, lam=float((0.05, 0.5, 2.0)[i % 3]),
+                        cfg=dict(outer_search=("ternary", "quadrature")[(i // 4) % 2])))
+    lres = pool.map(_task, [("locus", q) for q in lp_], chunksize=1)
+    out = {}
+    for tag, items, res in (("ccd", cp, cres), ("locus", lp_, lres)):
+        Mx = max(q["x"].shape[0] for q in items)
+        X = np.zeros((len(items), Mx, 8)); Y = np.zeros((len(items), Mx)); Bt = np.full((len(items), 8), np.nan)
+        for k, q in enumerate(items):
+            m, d = q["x"].shape
+            X[k, :m, :d] = q["x"]; Y[k, :m] = q["y"]
+            Bt[k, : len(res[k]["beta"])] = res[k]["beta"]
+        out[f"{tag}_x"], out[f"{tag}_y"], out[f"{tag}_beta"] = X, Y, Bt
+        out[f"{tag}_m"] = np.array([q["x"].shape[0] for q in items])
+        out[f"{tag}_d"] = np.array([q["x"].shape[1] for q in items])
+        out[f"{tag}_lam"] = np.array([q["lam"] for q in items])
+        out[f"{tag}_objective"] = np.array([r["objective"] for r in res])
+        for key in ("iterations", "objective_evals", "converged"):
+            out[f"{tag}_{key}"] = np.array([r[key] for r in res])
+    S0 = np.zeros((len(cp), 8))
+    for k, q in enumerate(cp):
+        S0[k, : len(q["start"])] = q["start"]
+    out["ccd_start"] = S0
+    out["ccd_frozen"] = np.array([-1 if q["frozen"] is None else q["frozen"] for q in cp])
+    out["locus_variant"] = np.array([q["cfg"]["outer_search"] == "quadrature" for q in lp_])
+    out["locus_D"] = np.array([r["D"] for r in lres]); out["locus_S"] = np.array([r["S"] for r in lres])
+    out["locus_status"] = np.array([r["status"] for r in lres])
+    np.savez_compressed(os.path.join(GOLDEN, "large.npz"), **out)
+    print("large.npz", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count())
@@ -584,7 +637,7 @@ def main():
     with Pool(a.procs) as pool:
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
-                         ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp)):
+                         ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp), ("large", gen_large)):
             if only is None or name in only:
                 fn(pool)
 

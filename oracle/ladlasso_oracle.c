@@ -49,7 +49,7 @@
 #include <pthread.h>
 
 #define ORC_MAX_D 8
-#define ORC_MAX_M 64
+#define ORC_MAX_M 1024
 
 /* ------------------------------------------------------------------ */
 /* problem + coordinate descent (ccd.py:126-206)                        */

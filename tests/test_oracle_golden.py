@@ -183,3 +183,23 @@ def test_certificate_oracle_matches_reference(oracle):
         got = oracle.is_axiswise_minimum(g["x"][i, :m, :d], g["y"][i, :m], max(float(g["lam"][i]), 1e-9),
                                          g["beta"][i, :d], None if sk < 0 else sk)
         assert got == bool(g["certified"][i]), i
+
+
+def test_large_problems_oracle_matches_reference(oracle):
+    """m up to 1000 rows: numpy's pairwise-sum recursion (n > 128), OpenBLAS ddot's 32-element
+    accumulator blocks (n >= 48) and dgemv_t rows, through ccd_descend and solve_locus."""
+    g = load_golden("large")
+    for i in range(len(g["ccd_lam"])):
+        m, d = int(g["ccd_m"][i]), int(g["ccd_d"][i])
+        fr = int(g["ccd_frozen"][i])
+        r = oracle.ccd_descend(g["ccd_x"][i, :m, :d], g["ccd_y"][i, :m], max(float(g["ccd_lam"][i]), 1e-9),
+                               g["ccd_start"][i, :d], None if fr < 0 else fr)
+        assert np.array_equal(r.beta, g["ccd_beta"][i, :d]) and r.objective == g["ccd_objective"][i], i
+        assert (r.iterations, r.objective_evals) == (g["ccd_iterations"][i], g["ccd_objective_evals"][i]), i
+    for i in range(len(g["locus_lam"])):
+        m, d = int(g["locus_m"][i]), int(g["locus_d"][i])
+        r = oracle.solve_locus(g["locus_x"][i, :m, :d], g["locus_y"][i, :m], max(float(g["locus_lam"][i]), 1e-9),
+                               outer_search="quadrature" if g["locus_variant"][i] else "ternary")
+        assert np.array_equal(r.beta, g["locus_beta"][i, :d]) and r.objective == g["locus_objective"][i], i
+        assert (r.iterations, r.objective_evals, r.descents, r.steps) == (
+            g["locus_iterations"][i], g["locus_objective_evals"][i], g["locus_D"][i], g["locus_S"][i]), i
