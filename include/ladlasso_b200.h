@@ -40,7 +40,7 @@ extern "C" {
 #define LAD_E_INVALID (-1)     /* bad shape / argument (InvalidInputError) */
 #define LAD_E_TOO_LARGE (-2)   /* brute caps exceeded (ProblemTooLargeError, brute.py:66-81) */
 #define LAD_E_CUDA (-3)        /* CUDA runtime failure */
-#define LAD_E_UNSUPPORTED (-4) /* n > 46 (fp32 mode: n > 31) or p > 8 */
+#define LAD_E_UNSUPPORTED (-4) /* p > 8, or n > 1023 (fp32 mode: n > 31; simplex: n > 46) */
 
 #define LAD_OUTER_TERNARY 0
 #define LAD_OUTER_QUADRATURE 1

@@ -20,6 +20,7 @@
 #include "lad_gen.cuh"
 #include "lad_locus.cuh"
 #include "lad_locus_warp.cuh"
+#include "lad_locus_block.cuh"
 
 #define LAD_VERSION 102
 
@@ -116,11 +117,14 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
         else v = make_warp_variant<8, 0>();
         return true;
     }
+    const bool block_ok = n >= 32 && n <= lad::BLK_NMAX && p <= 8;
+    if (block_ok && !(g_kernel_policy == LAD_KERNEL_THREAD && n <= 32)) {  // block per problem (32 <= n <= 1023)
+        v = Variant{lad::locus_block_kernel<8>, lad::BLK_NMAX, 8, lad::block_layout<8>(n, p).total, lad::BLK_THREADS, 1};
+        return true;
+    }
     if (thread_exact) v = make_thread_variant<10, 2, true>();
     else if (n <= 16 && p <= 4) v = make_thread_variant<16, 4, false>();
     else if (n <= 32 && p <= 8) v = make_thread_variant<32, 8, false>();
-    else if (n <= 46 && p <= 4) v = make_thread_variant<48, 4, false>();  // n + 1 <= 47: the modelled ddot range
-    else if (n <= 46 && p <= 8) v = make_thread_variant<48, 8, false>();
     else return false;
     return true;
 }
@@ -162,7 +166,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     if (!(prm->lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     Variant v;
     if (!pick_variant(n, p, v, f32))
-        return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : 46);
+        return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : lad::BLK_NMAX);
 
     if (g_num_sms == 0) {
         int dev;

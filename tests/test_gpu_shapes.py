@@ -68,11 +68,48 @@ def test_brute_beyond_32_rows(oracle, n, p):
 
 
 def test_shape_limits_are_reported():
-    X, Y, L = _problems(47, 2, 2, 5)
+    X, Y, L = _problems(1024, 2, 2, 5)
     with pytest.raises(lad.InvalidInputError):
         lad.solve_locus_batched(X, Y, L)
+    X, Y, L = _problems(47, 2, 2, 5)
     with pytest.raises(lad.InvalidInputError):
         lad.solve_lp_batched(X, Y, L)
     X32 = X[:, :32].astype(np.float32)
     with pytest.raises(lad.InvalidInputError):  # fp32 mode: warp kernel only (n <= 31)
         lad.solve_locus_batched(X32, Y[:, :32].astype(np.float32), L.astype(np.float32))
+
+
+def test_block_kernel_large_goldens():
+    """47 <= n <= 1023 (block per problem) against the reference: ccd_descend up to 1000 rows,
+    solve_locus (both variants, work counters) up to 256 rows (tests/golden/large.npz)."""
+    from conftest import load_golden
+
+    g = load_golden("large")
+    for i in range(len(g["ccd_lam"])):
+        m, d = int(g["ccd_m"][i]), int(g["ccd_d"][i])
+        if m <= 46:
+            continue
+        fr = int(g["ccd_frozen"][i])
+        r = lad.ccd_descend_batched(g["ccd_x"][i, :m, :d][None], g["ccd_y"][i, :m][None], g["ccd_lam"][i:i + 1],
+                                    g["ccd_start"][i, :d][None], lad.CcdConfig(), frozen=None if fr < 0 else fr)
+        assert np.array_equal(r.beta[0], g["ccd_beta"][i, :d]) and r.objective[0] == g["ccd_objective"][i], (i, m, d)
+        assert (r.iterations[0], r.objective_evals[0]) == (g["ccd_iterations"][i], g["ccd_objective_evals"][i])
+    for i in range(len(g["locus_lam"])):
+        m, d = int(g["locus_m"][i]), int(g["locus_d"][i])
+        v = "quadrature" if g["locus_variant"][i] else "ternary"
+        r = lad.solve_locus_batched(g["locus_x"][i, :m, :d][None], g["locus_y"][i, :m][None], g["locus_lam"][i:i + 1],
+                                    lad.LocusConfig(outer_search=v))
+        assert r.status[0] == 0
+        assert np.array_equal(r.beta[0], g["locus_beta"][i, :d]) and r.objective[0] == g["locus_objective"][i], (i, m)
+        assert (r.descents[0], r.steps[0]) == (g["locus_D"][i], g["locus_S"][i]), (i, m)
+        assert (r.iterations[0], r.objective_evals[0]) == (g["locus_iterations"][i], g["locus_objective_evals"][i])
+
+
+@pytest.mark.parametrize("n,p", [(47, 2), (64, 5), (100, 3), (129, 8), (200, 4), (333, 1), (1023, 2)])
+def test_block_kernel_against_oracle(oracle, n, p):
+    X, Y, L = _problems(n, p, 3, 4000 + n * p)
+    r = lad.solve_locus_batched(X, Y, L)
+    o = oracle.solve_locus_batch(X, Y, L)
+    assert np.array_equal(r.status, o["status"])
+    assert np.array_equal(r.beta, o["beta"]) and np.array_equal(r.objective, o["objective"]), (n, p)
+    assert np.array_equal(r.steps, o["steps"]) and np.array_equal(r.descents, o["descents"]), (n, p)
