@@ -497,3 +497,11 @@ def is_axiswise_minimum(spec, beta, skip=None, tol: float = 1e-9) -> bool:
         raise DimensionMismatchError(f"beta has shape {b.shape}, problem has {X.shape[2]} variables")
     return bool(axiswise_minimum_batched(X, y, lam, b[None], -1 if skip is None else int(skip), tol,
                                          lambda_floor=floor)[0])
+
+
+def validate_result(spec, result, rtol: float = 1e-12) -> None:
+    """Drop-in for ``ladlasso.model.validate_result`` (model.py:180-186): the stored objective must
+    reproduce a fresh evaluation (on the GPU) within rtol."""
+    f = evaluate_objective(spec, result.beta)
+    if abs(result.objective - f) > rtol * max(1.0, abs(f)):
+        raise InvalidInputError(f"stored objective {result.objective!r} does not reproduce {f!r}")
