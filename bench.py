@@ -155,7 +155,7 @@ def run_reference(a, rank, world):
     if rank != 0:
         return
     import torch  # noqa: F401  (device generator provides the identical problem bytes)
-    from paper_2510_15649_b200 import generate as G
+    from paper_2510_15649_b200 import configgen as G
 
     per_step = max(1, min(a.cpu_sample, 256))  # 4,096 solves (~1.3 s on 16 threads) per step
     times, solves = [], 0
@@ -192,7 +192,7 @@ class Workload:
 
     def _build(self, config, a, world, rank, dev):
         import torch
-        from paper_2510_15649_b200 import generate as G
+        from paper_2510_15649_b200 import configgen as G
         from paper_2510_15649_b200.distributed import block_for_step
 
         self.config = config
@@ -277,7 +277,7 @@ def run_aux(a, world, rank, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import paper_2510_15649_b200 as lad
-    from paper_2510_15649_b200 import _lib, generate as G
+    from paper_2510_15649_b200 import _lib, configgen as G
     from paper_2510_15649_b200.solver import fp64_peak_tflops
 
     if a.solver == "lp":

@@ -172,6 +172,13 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
         int dev;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+        // keep the per-call scratch (seen lists, counters) mapped between calls instead of
+        // returning it to the OS at every synchronize (default release threshold 0)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = 2ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     if (v.smem > 48 * 1024) CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
     int per_sm = 0;

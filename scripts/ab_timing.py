@@ -8,7 +8,7 @@ sys.path.insert(0, '.')
 from paper_2510_15649_b200 import _build, _lib
 _build.LIB = sys.argv[1]
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import generate as G
+from paper_2510_15649_b200 import configgen as G
 config = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 16
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3

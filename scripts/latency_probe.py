@@ -1,7 +1,7 @@
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import generate as G, _lib
+from paper_2510_15649_b200 import configgen as G, _lib
 X, Y, L = G.generate(0, 256, seed=15649)
 cfg = lad.LocusConfig()
 # warm clocks

@@ -3,7 +3,7 @@ import sys, argparse
 import torch
 sys.path.insert(0, '.')
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import generate as G
+from paper_2510_15649_b200 import configgen as G
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--B", type=int, default=4096)

@@ -3,7 +3,7 @@ import sys, time
 import torch
 sys.path.insert(0, '.')
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import generate as G
+from paper_2510_15649_b200 import configgen as G
 
 def run(config, B, variant="ternary", lam=None):
     X, Y, L = G.generate(config, B, seed=1)

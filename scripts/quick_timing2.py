@@ -2,7 +2,7 @@ import sys, time, subprocess
 import torch
 sys.path.insert(0, '.')
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import generate as G, _lib
+from paper_2510_15649_b200 import configgen as G, _lib
 print(subprocess.run(["nvidia-smi","--query-gpu=clocks.sm,clocks.max.sm,power.draw","--format=csv,noheader"],capture_output=True,text=True).stdout.strip())
 def run(config, B, variant="ternary", policy=0, reps=2):
     _lib.set_kernel_policy(policy)

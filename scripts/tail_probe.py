@@ -4,7 +4,7 @@ import numpy as np
 import torch
 sys.path.insert(0, '.')
 import paper_2510_15649_b200 as lad
-from paper_2510_15649_b200 import _lib, generate as G
+from paper_2510_15649_b200 import _lib, configgen as G
 from paper_2510_15649_b200.distributed import block_for_step
 LAMBDA_GRID = 10.0 ** np.linspace(-2.0, 1.0, 16)
 blk = 1 << 14

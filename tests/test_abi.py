@@ -70,3 +70,16 @@ def test_host_validation_raises_reference_errors():
         locus_params(lad.LocusConfig(outer_axis=3), d=2)
     with pytest.raises(lad.InvalidInputError):
         locus_params(lad.LocusConfig(inner=lad.CcdConfig(line_search="ternary")))
+
+
+def test_package_namespace_is_consistent():
+    """The reference's names resolve to the reference's objects (no submodule shadowing)."""
+    import types
+
+    import paper_2510_15649_b200 as lad
+    from paper_2510_15649_b200 import configgen, synth
+
+    assert lad.generate is synth.generate and callable(lad.generate)
+    assert isinstance(configgen, types.ModuleType) and hasattr(configgen, "CONFIG_SHAPES")
+    for name in lad.__all__:
+        assert not isinstance(getattr(lad, name), types.ModuleType), name

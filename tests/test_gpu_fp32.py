@@ -22,7 +22,7 @@ if not torch.cuda.is_available():
 
 import paper_2510_15649_b200 as lad  # noqa: E402
 from paper_2510_15649_b200 import _lib  # noqa: E402
-from paper_2510_15649_b200 import generate as G  # noqa: E402
+from paper_2510_15649_b200 import configgen as G  # noqa: E402
 
 
 def _np(a):

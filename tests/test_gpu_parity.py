@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 import paper_2510_15649_b200 as lad  # noqa: E402
-from paper_2510_15649_b200 import generate as G  # noqa: E402
+from paper_2510_15649_b200 import configgen as G  # noqa: E402
 
 
 def _np(a):
