@@ -14,7 +14,7 @@ The dataset CSV format is the reference's: header ``x1,...,xd,y``, one point
 per row, shortest round-trip float repr; plus a ``.meta.json`` sidecar.
 
 The BASELINE.json config generators (configs 0-4) run on the device instead
-(generate.py); this module exists for the reference-facing CLI.
+(configgen.py); this module exists for the reference-facing CLI.
 """
 
 from __future__ import annotations
