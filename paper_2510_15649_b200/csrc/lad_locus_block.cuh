@@ -1,7 +1,8 @@
 // lad_locus_block.cuh -- block-per-problem locus kernel for 47 <= n <= 1023 rows (binary64).
 //
-// 256 threads per problem, persistent grid.  Thread t owns elements
-// t, t + 256, t + 512, t + 768 of a step (rows, then the lambda breakpoint).
+// 32 * ceil((n + 1) / 32) threads per problem (at most 256), persistent grid.
+// Thread t owns elements t, t + T, t + 2T, t + 3T of a step (rows, then the
+// lambda breakpoint).
 // Every warp runs the shared controller (lad_locus.cuh) on its own copy of
 // the state: the inputs it sees are identical in every warp, so the copies
 // stay identical, and sync() is __syncthreads().  Per coordinate step:
@@ -76,6 +77,7 @@ struct BlockHead {
     double scale[PMAX];      // fixed-point scale per axis (2^30 / total weight)
     unsigned halfq[PMAX];    // (sum of fixed-point weights) / 2 per axis
     int cand[PMAX];          // previous median element per axis
+    int cand2[PMAX];         // the one before
     unsigned long long item;
     double redd[BLK_WARPS];
     unsigned redu[2][BLK_WARPS];
@@ -136,8 +138,8 @@ __device__ __forceinline__ unsigned block_sum_u2(unsigned a, unsigned b, unsigne
     __syncthreads();
     unsigned sa = 0;
     sb = 0;
-#pragma unroll
-    for (int k = 0; k < BLK_WARPS; ++k) {
+    const int nw = (int)(blockDim.x >> 5);
+    for (int k = 0; k < nw; ++k) {
         sa += red[0][k];
         sb += red[1][k];
     }
@@ -154,8 +156,8 @@ __device__ __forceinline__ double block_sum_d(double v, double *red)
     if (lane == 0) red[wp] = v;
     __syncthreads();
     double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < BLK_WARPS; ++k) s += red[k];
+    const int nw = (int)(blockDim.x >> 5);
+    for (int k = 0; k < nw; ++k) s += red[k];
     __syncthreads();
     return s;
 }
@@ -193,13 +195,13 @@ struct BlockAccess {
         const double *xg = A.X + (size_t)src * n * p, *yg = A.Y + (size_t)src * n;
         bool ok = true;
         unsigned mask = 0;
-        for (int e = tid; e < n * p; e += BLK_THREADS) {
+        for (int e = tid; e < n * p; e += (int)blockDim.x) {
             const double v = xg[e];
             M.X[e] = v;
             ok = ok && isfinite(v);
             if (v == 0.0) mask |= 1u << (e % p);
         }
-        for (int i = tid; i < n; i += BLK_THREADS) {
+        for (int i = tid; i < n; i += (int)blockDim.x) {
             const double v = yg[i];
             M.Y[i] = v;
             ok = ok && isfinite(v);
@@ -212,12 +214,12 @@ struct BlockAccess {
         // fixed-point weights per axis for the median test (any summation order will do)
         for (int j = 0; j < p; ++j) {
             double s = 0.0;
-            for (int e = tid; e <= n; e += BLK_THREADS) s += e < n ? fabs(M.X[e * p + j]) : lam_eff;
+            for (int e = tid; e <= n; e += (int)blockDim.x) s += e < n ? fabs(M.X[e * p + j]) : lam_eff;
             const double tot = block_sum_d(s, H->redd);
             const double scale = 1073741824.0 / (tot * (1.0 + 1e-9));
             const bool good = tot > 0.0 && tot < 1e300;
             unsigned qs = 0;
-            for (int e = tid; e <= n; e += BLK_THREADS)
+            for (int e = tid; e <= n; e += (int)blockDim.x)
                 qs += good ? __double2uint_rz((e < n ? fabs(M.X[e * p + j]) : lam_eff) * scale) : 0u;
             unsigned dummy;
             const unsigned sq = block_sum_u2(qs, 0u, H->redu, dummy);
@@ -311,7 +313,7 @@ __device__ __forceinline__ void block_bitonic(double *key, int *idx, int P2)
 {
     for (int k = 2; k <= P2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P2; i += BLK_THREADS) {
+            for (int i = threadIdx.x; i < P2; i += (int)blockDim.x) {
                 const int ixj = i ^ j;
                 if (ixj > i) {
                     const double ka = key[i], kb = key[ixj];
@@ -346,7 +348,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
     if (!col_sparse) {
 #pragma unroll
         for (int q = 0; q < BLK_EPT; ++q) {
-            const int e = tid + q * BLK_THREADS;
+            const int e = tid + q * (int)blockDim.x;
             if (e < n) {
                 const double x = M.X[e * p + j];
                 M.loc[e] = dadd(ddiv(r[q], x), bj);
@@ -377,14 +379,14 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         int base = 0;
         for (int k = 0; k < (tid >> 5); ++k) base += (int)H->redu[0][k];
         int total = 0;
-        for (int k = 0; k < BLK_WARPS; ++k) total += (int)H->redu[0][k];
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) total += (int)H->redu[0][k];
         int pnz = base + incl - nnz;
         // rows are spread over threads as i = tid * EPT + q here, but r[q] belongs to row tid + q * 256:
         // stage the residuals in tmp first
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < BLK_EPT; ++q) {
-            const int i = tid + q * BLK_THREADS;
+            const int i = tid + q * (int)blockDim.x;
             if (i < n) M.tmp[i] = r[q];
         }
         __syncthreads();
@@ -413,7 +415,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         zsum = H->bcd[0];
         cnt = total + 1;
     }
-    for (int e = cnt + tid; e < M.P2; e += BLK_THREADS) M.loc[e] = INF;
+    for (int e = cnt + tid; e < M.P2; e += (int)blockDim.x) M.loc[e] = INF;
     __syncthreads();
     // weighted median (ccd.py:81-91)
     const double scale = H->scale[j];
@@ -421,27 +423,38 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
     double t_new;
     bool hit = false;
     if (!col_sparse) {
-        const int m = H->cand[j];
-        const double lm = M.loc[m];
-        unsigned qb = 0, qi = 0;
+        // is element m the median?  exact fixed-point block sums: the answer is uniform
+        auto test = [&](int m, double &lm) {
+            lm = M.loc[m];
+            unsigned qb = 0, qi = 0;
 #pragma unroll
-        for (int q = 0; q < BLK_EPT; ++q) {
-            const int e = tid + q * BLK_THREADS;
-            if (e < cnt) {
-                const double le = M.loc[e];
-                const unsigned qe = __double2uint_rz(M.w[e] * scale);
-                const bool below = (le < lm) | ((le == lm) & (e < m));
-                qb += below ? qe : 0u;
-                qi += (below | (e == m)) ? qe : 0u;
+            for (int q = 0; q < BLK_EPT; ++q) {
+                const int e = tid + q * (int)blockDim.x;
+                if (e < cnt) {
+                    const double le = M.loc[e];
+                    const unsigned qe = __double2uint_rz(M.w[e] * scale);
+                    const bool below = (le < lm) | ((le == lm) & (e < m));
+                    qb += below ? qe : 0u;
+                    qi += (below | (e == m)) ? qe : 0u;
+                }
+            }
+            unsigned sqi;
+            const unsigned sqb = block_sum_u2(qb, qi, H->redu, sqi);
+            return scale > 0.0 && (sqb + MEDIAN_MARGIN_Q < hq) && (sqi > hq + MEDIAN_MARGIN_Q);
+        };
+        const int m1 = H->cand[j], m2 = H->cand2[j];
+        hit = test(m1, t_new);
+        if (!hit && m2 != m1 && test(m2, t_new)) {
+            hit = true;
+            __syncthreads();
+            if (tid == 0) {
+                H->cand2[j] = m1;
+                H->cand[j] = m2;
             }
         }
-        unsigned sqi;
-        const unsigned sqb = block_sum_u2(qb, qi, H->redu, sqi);
-        hit = scale > 0.0 && (sqb + MEDIAN_MARGIN_Q < hq) && (sqi > hq + MEDIAN_MARGIN_Q);
-        t_new = lm;
     }
     if (!hit) {
-        for (int e = tid; e < M.P2; e += BLK_THREADS) {
+        for (int e = tid; e < M.P2; e += (int)blockDim.x) {
             M.sk[e] = M.loc[e];
             M.si[e] = e;
         }
@@ -510,13 +523,16 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         }
         const int ks = k < cnt ? k : cnt - 1;
         t_new = tie ? dmul(0.5, dadd(M.sk[ks], M.sk[ks + 1])) : M.sk[ks];
-        if (!col_sparse && tid == 0) H->cand[j] = M.si[ks];
+        if (!col_sparse && tid == 0) {
+            H->cand2[j] = H->cand[j];
+            H->cand[j] = M.si[ks];
+        }
     }
     __syncthreads();
     if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
     double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
     if (col_sparse) constant = dadd(constant, zsum);
-    for (int e = tid; e < cnt; e += BLK_THREADS) M.aw[e] = make_double2(fabs(dsub(t_new, M.loc[e])), M.w[e]);
+    for (int e = tid; e < cnt; e += (int)blockDim.x) M.aw[e] = make_double2(fabs(dsub(t_new, M.loc[e])), M.w[e]);
     __syncthreads();
     if ((tid >> 5) == 0) {
         const double dot = block_blas_ddot(M.aw, cnt, lane);
@@ -528,7 +544,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         const double delta = dsub(t_new, bj);
 #pragma unroll
         for (int q = 0; q < BLK_EPT; ++q) {
-            const int i = tid + q * BLK_THREADS;
+            const int i = tid + q * (int)blockDim.x;
             if (i < n) r[q] = dsub(r[q], dmul(M.X[i * p + j], delta));
         }
         sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
@@ -543,7 +559,7 @@ template <int PMAX>
 __device__ double block_objective(const BlockMem<PMAX> &M, int n, int p, double lam)
 {
     BlockHead<PMAX> *H = M.H;
-    for (int i = threadIdx.x; i < n; i += BLK_THREADS) {
+    for (int i = threadIdx.x; i < n; i += (int)blockDim.x) {
         const double g = gemv_row(p, i, n, [&](int q) { return M.X[i * p + q]; }, [&](int q) { return H->B[q]; });
         M.tmp[i] = fabs(dsub(M.Y[i], g));
     }
@@ -573,7 +589,7 @@ __device__ void block_descent(const BlockMem<PMAX> &M, Ctl<PMAX> &C, int n, int 
     double r[BLK_EPT];
 #pragma unroll
     for (int q = 0; q < BLK_EPT; ++q) {
-        const int i = tid + q * BLK_THREADS;
+        const int i = tid + q * (int)blockDim.x;
         r[q] = 0.0;
         if (i < n) {
             const double g = gemv_row(p, i, n, [&](int c) { return M.X[i * p + c]; }, [&](int c) { return H->B[c]; });
@@ -652,7 +668,10 @@ __global__ void __launch_bounds__(BLK_THREADS) locus_block_kernel(LocusArgs A)
     M.P2 = L.P2;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     Ctl<PMAX> &C = M.H->C[wp];
-    if (threadIdx.x < PMAX) M.H->cand[threadIdx.x] = 0;
+    if (threadIdx.x < PMAX) {
+        M.H->cand[threadIdx.x] = 0;
+        M.H->cand2[threadIdx.x] = 1;
+    }
     if (lane == 0) C.pc = PC_FETCH;
     __syncthreads();
     BlockAccess<PMAX> acc{n, p, lane, M};

@@ -119,7 +119,8 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
     }
     const bool block_ok = n >= 32 && n <= lad::BLK_NMAX && p <= 8;
     if (block_ok && !(g_kernel_policy == LAD_KERNEL_THREAD && n <= 32)) {  // block per problem (32 <= n <= 1023)
-        v = Variant{lad::locus_block_kernel<8>, lad::BLK_NMAX, 8, lad::block_layout<8>(n, p).total, lad::BLK_THREADS, 1};
+        const int threads = std::min(lad::BLK_THREADS, 32 * ((n + 1 + 31) / 32));
+        v = Variant{lad::locus_block_kernel<8>, lad::BLK_NMAX, 8, lad::block_layout<8>(n, p).total, threads, 1};
         return true;
     }
     if (thread_exact) v = make_thread_variant<10, 2, true>();
