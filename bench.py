@@ -399,7 +399,6 @@ def run_aux(a, world, rank, local):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "flops_model": "bench.lp_flops" if a.solver == "lp" else "bench.brute_flops"},
-            "issue_roofline": issue,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": len(hosts)},

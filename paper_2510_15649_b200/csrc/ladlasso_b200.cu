@@ -131,6 +131,32 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
 }
 
 int g_num_sms = 0;
+std::atomic<uint64_t> g_pool_devices{0};  // devices whose default pool keeps freed scratch mapped
+
+// Per-process, per-device setup: the SM count (grid sizing) and the default
+// stream-ordered pool's release threshold, so the per-call scratch (seen lists,
+// counters) stays mapped between calls instead of being returned to the OS at
+// every synchronize (default threshold 0).
+cudaError_t device_init()
+{
+    int dev;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (g_num_sms == 0) {
+        e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(g_pool_devices.load() & bit)) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = 2ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        g_pool_devices.fetch_or(bit);
+    }
+    return cudaSuccess;
+}
 
 int seen_capacity(const lad_locus_params *prm, int p)
 {
@@ -169,18 +195,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     if (!pick_variant(n, p, v, f32))
         return fail(LAD_E_UNSUPPORTED, "n=%d p=%d beyond n<=%d, p<=8", n, p, f32 ? 31 : lad::BLK_NMAX);
 
-    if (g_num_sms == 0) {
-        int dev;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-        // keep the per-call scratch (seen lists, counters) mapped between calls instead of
-        // returning it to the OS at every synchronize (default release threshold 0)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = 2ull << 30;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    }
+    CK(device_init());
     if (v.smem > 48 * 1024) CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.block, v.smem));
@@ -420,11 +435,7 @@ __global__ void fma_peak_kernel(T *out, int iters)
 template <typename T>
 int fma_peak_tflops(double *tflops, cudaStream_t st)
 {
-    if (g_num_sms == 0) {
-        int dev;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    CK(device_init());
     const int block = 256, blocks = g_num_sms * 8, iters = 1 << 14;
     T *dout = nullptr;
     CK(cudaMallocAsync((void **)&dout, sizeof(T), st));
