@@ -88,6 +88,17 @@ class ClockSampler:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
+        # nvidia-smi's start-up (driver attach, first query) can pause the GPU briefly: let it
+        # finish before the timed region begins (sampling then continues through the region)
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 5.0:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                break
+            time.sleep(0.05)
+        time.sleep(0.3)
         return self
 
     def __exit__(self, *exc):
