@@ -355,51 +355,15 @@ __device__ __forceinline__ void sparse_column(WarpShared<PMAX, T> *W, int lane, 
     cnt = k + 1;
 }
 
-// Weighted median, skip test, v_new and strict accept of one coordinate step
-// (ccd.py:81-91, :172-191), given this lane's breakpoint (loc, w).  CNTC > 0:
-// compile-time breakpoint count (dense column in a compile-time-n kernel),
-// so the reduction trees, tail lengths and bounds are constants.
+// Weighted median by ordering (the fast path's miss): stable order of (location,
+// index) -- cached permutation, odd-even repair, bitonic network -- then the
+// cumulative-weight decision.
 template <int PMAX, int CNTC, typename T>
-__device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j, T lam,
-                                              bool cacheable, int cnt_rt, T loc, T w, T zsum, bool have_zero,
-                                              bool row, T xij, T bj, T &r, T &f_cur, T &sum_abs_b,
-                                              uint32_t &perm_valid)
+__device__ __forceinline__ T median_by_order(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j,
+                                             bool cacheable, int cnt_rt, T loc, T w, uint32_t &perm_valid)
 {
     const int cnt = CNTC > 0 ? CNTC : cnt_rt;
-    // Fast path (dense columns): the weighted median is usually the same
-    // element as at this axis' previous step.  Element m is the median iff the
-    // weight of the elements ordered before it, W_below, satisfies
-    // W_below < total/2 <= W_below + w_m (in numpy's sequential cumsum).  With
-    // the weights in 2^-30-of-total fixed point (floor, <= 32 units of error
-    // per sum) both sums are exact warp reductions, and a decision made with
-    // a 2^14-unit (1.5e-5 * total) margin on both sides is the reference's
-    // decision; it also excludes the 1e-12 * total midpoint tie.  Otherwise
-    // the full order + scan below decides.
     T t_new;
-    bool hit = false;
-    if (cacheable) {
-        const unsigned q = W->wq[j][lane];
-        const unsigned hq = W->halfq[j];
-        const int m1 = W->cand[j];
-        // is element m the median?  (exact integer sums: the answer is warp-uniform)
-        auto test = [&](int m, T &lm) {
-            lm = shfl_t(loc, m);
-            const bool below = (loc < lm) | ((loc == lm) & (lane < m));
-            const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
-            const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
-            return (qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q);
-        };
-        hit = test(m1, t_new);
-        if (!hit) {
-            const int m2 = W->cand2[j];
-            if (m2 != m1 && test(m2, t_new)) {
-                hit = true;
-                W->cand2[j] = m1;  // identical value from every lane
-                W->cand[j] = m2;
-            }
-        }
-    }
-    if (!hit) {
     // stable order by (location, index).  The order is unique, so if this
     // axis' permutation from its previous evaluation is still sorted under the
     // new locations it is the answer; otherwise odd-even transposition rounds
@@ -465,6 +429,68 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
         __syncwarp();
         W->cand[j] = mnew;
     }
+    return t_new;
+}
+
+// Out-of-line copy for p <= 5: the miss path runs on ~10% of steps, and keeping it
+// out of the step body keeps the hot path compact in the instruction cache
+// (config 2: +5%).  For p = 8 misses are frequent enough that the call costs more.
+template <int PMAX, int CNTC, typename T>
+__device__ __noinline__ T median_by_order_call(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j,
+                                               bool cacheable, int cnt_rt, T loc, T w, uint32_t &perm_valid)
+{
+    return median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
+}
+
+// Weighted median, skip test, v_new and strict accept of one coordinate step
+// (ccd.py:81-91, :172-191), given this lane's breakpoint (loc, w).  CNTC > 0:
+// compile-time breakpoint count (dense column in a compile-time-n kernel),
+// so the reduction trees, tail lengths and bounds are constants.
+template <int PMAX, int CNTC, typename T>
+__device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j, T lam,
+                                              bool cacheable, int cnt_rt, T loc, T w, T zsum, bool have_zero,
+                                              bool row, T xij, T bj, T &r, T &f_cur, T &sum_abs_b,
+                                              uint32_t &perm_valid)
+{
+    const int cnt = CNTC > 0 ? CNTC : cnt_rt;
+    // Fast path (dense columns): the weighted median is usually the same
+    // element as at this axis' previous step.  Element m is the median iff the
+    // weight of the elements ordered before it, W_below, satisfies
+    // W_below < total/2 <= W_below + w_m (in numpy's sequential cumsum).  With
+    // the weights in 2^-30-of-total fixed point (floor, <= 32 units of error
+    // per sum) both sums are exact warp reductions, and a decision made with
+    // a 2^14-unit (1.5e-5 * total) margin on both sides is the reference's
+    // decision; it also excludes the 1e-12 * total midpoint tie.  Otherwise
+    // the full order + scan below decides.
+    T t_new;
+    bool hit = false;
+    if (cacheable) {
+        const unsigned q = W->wq[j][lane];
+        const unsigned hq = W->halfq[j];
+        const int m1 = W->cand[j];
+        // is element m the median?  (exact integer sums: the answer is warp-uniform)
+        auto test = [&](int m, T &lm) {
+            lm = shfl_t(loc, m);
+            const bool below = (loc < lm) | ((loc == lm) & (lane < m));
+            const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
+            const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
+            return (qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q);
+        };
+        hit = test(m1, t_new);
+        if (!hit) {
+            const int m2 = W->cand2[j];
+            if (m2 != m1 && test(m2, t_new)) {
+                hit = true;
+                W->cand2[j] = m1;  // identical value from every lane
+                W->cand[j] = m2;
+            }
+        }
+    }
+    if (!hit) {
+        if constexpr (PMAX <= 5)
+            t_new = median_by_order_call<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
+        else
+            t_new = median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
     }
     if (fabs(dsub(t_new, bj)) <= dmul(T(1e-14), dadd(T(1), fabs(bj)))) return;  // ccd.py:172
     T constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
