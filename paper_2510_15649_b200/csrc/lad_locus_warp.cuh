@@ -537,6 +537,27 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     }
 }
 
+template <typename T>
+struct StepState {
+    T r, f_cur, sum_abs_b;
+};
+
+// A step on a column with zero entries (compacted breakpoints).  Out of line:
+// such columns are rare, and a second inlined copy of the median/update code
+// would bloat the hot step body.  State goes in and out by value (registers).
+template <int PMAX, typename T>
+__device__ __noinline__ StepState<T> sparse_step(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int n, int j,
+                                                 T lam, bool row, T xij, T bj, StepState<T> st)
+{
+    T loc, w, zsum;
+    int cnt;
+    sparse_column<PMAX, T>(W, lane, n, st.r, xij, bj, lam, loc, w, cnt, zsum);
+    uint32_t unused = 0;  // sparse columns never use the order cache
+    median_update<PMAX, 0, T>(W, lane, inv_mask, j, lam, false, cnt, loc, w, zsum, true, row, xij, bj, st.r, st.f_cur,
+                              st.sum_abs_b, unused);
+    return st;
+}
+
 // One exact coordinate step on axis j (ccd.py:160-193), all lanes in lock-step.
 // NC > 0: compile-time row count (config shapes); NC == 0: runtime n_rt.
 template <int PMAX, int NC, typename T>
@@ -563,7 +584,12 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
         const T w = row ? fabs(xij) : (lane == n ? lam : T(0));
         median_update<PMAX, (NC > 0 ? NC + 1 : 0), T>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, T(0), false,
                                                       row, xij, bj, r, f_cur, sum_abs_b, perm_valid);
-    } else {
+    } else if constexpr (PMAX <= 5) {
+        const StepState<T> st = sparse_step<PMAX, T>(W, lane, inv_mask, n, j, lam, row, xij, bj, {r, f_cur, sum_abs_b});
+        r = st.r;
+        f_cur = st.f_cur;
+        sum_abs_b = st.sum_abs_b;
+    } else {  // p = 8: inline (measured faster for the config-4 shape)
         T loc, w, zsum;
         int cnt;
         sparse_column<PMAX, T>(W, lane, n, r, xij, bj, lam, loc, w, cnt, zsum);
