@@ -4,8 +4,10 @@
 Workload (BASELINE.json configs[2], the largest n=30/p=5 configuration): the
 lambda path -- 2^20 datasets generated as config 0, each solved at a 16-point
 log-spaced lambda grid 1e-2..1e1 (cold solves: the reference has no warm-start
-knob).  One bench *step* = one block of datasets (default 2^14)
-x all 16 lambdas = 262,144 solves per GPU; the whole config is 64 such steps.
+knob), with both outer searches as the config states.  One bench
+*step* = one block of datasets (default 2^14) x all 16 lambdas x {ternary,
+quadrature} = 524,288 solves per GPU (two launches over the same resident
+datasets); the whole config is 64 such steps.
 Weak scaling: rank r of N solves block (step * N + r).
 
 Timing: per-step CUDA events on the launching stream, L2 flushed (256 MiB
@@ -47,7 +49,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--block", type=int, default=1 << 14, help="datasets per step per GPU (x16 lambdas)")
-    ap.add_argument("--variant", choices=["ternary", "quadrature"], default="ternary")
+    ap.add_argument("--variant", choices=["ternary", "quadrature", "both"], default=None,
+                    help="outer search; default: both for config 2 (as BASELINE states), quadrature for "
+                         "config 3, ternary otherwise")
     ap.add_argument("--cpu-sample", type=int, default=2048,
                     help="CPU baseline sample: datasets (x16 lambdas) for config 2, problems otherwise (~10 s of CPU)")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -146,8 +150,14 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_cpu_sample(X, Y, datasets, variant):
-    """Oracle (CPU restatement of the reference) on datasets x 16 lambdas, all host threads."""
+def variants_of(a, config):
+    """Outer searches one step runs (config 2 states both, config 3 quadrature)."""
+    v = a.variant or {2: "both", 3: "quadrature"}.get(config, "ternary")
+    return ["ternary", "quadrature"] if v == "both" else [v]
+
+
+def run_cpu_sample(X, Y, datasets, variants):
+    """Oracle (CPU restatement of the reference) on datasets x 16 lambdas x variants, all host threads."""
     from oracle import oracle as O
 
     O.build()
@@ -156,9 +166,9 @@ def run_cpu_sample(X, Y, datasets, variant):
     L = np.tile(LAMBDA_GRID, datasets)
     nth = cpu_threads()
     t0 = time.perf_counter()
-    r = O.solve_locus_batch(Xs, Ys, L, nthreads=nth, outer_search=variant)
+    r = [O.solve_locus_batch(Xs, Ys, L, nthreads=nth, outer_search=v) for v in variants]
     dt = time.perf_counter() - t0
-    return r, dt, nth, Xs.shape[0]
+    return r, dt, nth, Xs.shape[0] * len(variants)
 
 
 def run_reference(a, rank, world):
@@ -168,12 +178,13 @@ def run_reference(a, rank, world):
     import torch  # noqa: F401  (device generator provides the identical problem bytes)
     from paper_2510_15649_b200 import configgen as G
 
-    per_step = max(1, min(a.cpu_sample, 256))  # 4,096 solves (~1.3 s on 16 threads) per step
+    variants = variants_of(a, 2)
+    per_step = max(1, min(a.cpu_sample, 256 // len(variants)))  # 4,096 solves (~1.3 s on 16 threads) per step
     times, solves = [], 0
     for s in range(a.warmup + a.steps):
         Xd, Yd, _ = G.generate(2, per_step, seed=SEED, first=(s * a.block) % TOTAL_DATASETS)
         X, Y = Xd.cpu().numpy(), Yd.cpu().numpy()
-        _, dt, nth, ns = run_cpu_sample(X, Y, per_step, a.variant)
+        _, dt, nth, ns = run_cpu_sample(X, Y, per_step, variants)
         if s >= a.warmup:
             times.append(dt)
             solves += ns
@@ -183,10 +194,11 @@ def run_reference(a, rank, world):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device Philox generator, BASELINE config 2 distributions)",
-            "config": {"workload": "config2_lambda_path", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
-                       "variant": a.variant, "solves_per_step": per_step * 16},
+            "config": {"workload": "config2", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
+                       "variant": "+".join(variants), "solves_per_step": per_step * 16 * len(variants)},
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": nth, "kind": "port",
-                             "sample": f"{per_step} config-2 datasets x 16 lambdas per step, {a.steps} timed steps"},
+                             "sample": f"{per_step} config-2 datasets x 16 lambdas x {'+'.join(variants)} per step, "
+                                       f"{a.steps} timed steps, CPU oracle (C restatement of solve_locus)"},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -207,7 +219,7 @@ class Workload:
         from paper_2510_15649_b200.distributed import block_for_step
 
         self.config = config
-        self.variant = a.variant if config != 3 else "quadrature"
+        self.variants = variants_of(a, config)
         self.n, self.p = G.CONFIG_SHAPES[config]
         self.dev = dev
         self.data_index = None
@@ -217,7 +229,7 @@ class Workload:
         if config == 2:
             blk = a.block
             self.desc = (f"config 2 lambda path: 2^20 datasets (n=30, p=5, config-0 distributions) x 16 lambdas "
-                         f"1e-2..1e1; step = {blk} datasets x 16 lambdas")
+                         f"1e-2..1e1; step = {blk} datasets x 16 lambdas x {'+'.join(self.variants)}")
             for s in range(nsteps):
                 first = block_for_step(s, world, rank, TOTAL_DATASETS // blk) * blk
                 X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
@@ -442,8 +454,8 @@ def main():
     from paper_2510_15649_b200.solver import fp32_peak_tflops, fp64_peak_tflops
 
     wl = Workload(a.config, a, world, rank, dev)
-    cfg = lad.LocusConfig(outer_search=wl.variant)
-    solves_per_step = wl.solves
+    cfgs = [lad.LocusConfig(outer_search=v) for v in wl.variants]
+    solves_per_step = wl.solves * len(cfgs)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
     peak = fp32_peak_tflops() if a.dtype == "f32" else fp64_peak_tflops()
@@ -456,7 +468,7 @@ def main():
 
     def solve(s):
         X, Y, L = wl.inputs(s)
-        return lad.solve_locus_batched(X, Y, L, cfg, data_index=wl.data_index)
+        return [lad.solve_locus_batched(X, Y, L, c, data_index=wl.data_index) for c in cfgs]
 
     for s in range(a.warmup):
         solve(s)
@@ -472,7 +484,7 @@ def main():
             evs[k][0].record(stream)
             r = solve(a.warmup + k)
             evs[k][1].record(stream)
-            results.append(r)
+            results.extend(r)
         barrier()
     gpu_launches = _lib.kernel_launches() - launches0
     clocks = clk.summary()
@@ -510,19 +522,21 @@ def main():
         hidx_np = hidx.numpy()
     m_warm = min(1024, host[0][2].shape[0])  # untimed warm-up of the host-buffer path (allocator, first call)
     lad.solve_locus_batched(host[0][0][: m_warm if hidx_np is None else host[0][0].shape[0]],
-                            host[0][1][: m_warm if hidx_np is None else host[0][1].shape[0]], host[0][2][:m_warm], cfg,
-                            data_index=None if hidx_np is None else hidx_np[:m_warm])
+                            host[0][1][: m_warm if hidx_np is None else host[0][1].shape[0]], host[0][2][:m_warm],
+                            cfgs[0], data_index=None if hidx_np is None else hidx_np[:m_warm])
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        r = lad.solve_locus_batched(host[k][0], host[k][1], host[k][2], cfg, data_index=hidx_np)
+        for c in cfgs:  # each variant is one public-API call with its own H2D and D2H
+            lad.solve_locus_batched(host[k][0], host[k][1], host[k][2], c, data_index=hidx_np)
     barrier()
     e2e_elapsed = time.perf_counter() - t0
     te = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_steps * solves_per_step / float(te.item())
-    h2d = host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes + (hidx_np.nbytes if hidx_np is not None else 0)
+    h2d = len(cfgs) * (host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes +
+                       (hidx_np.nbytes if hidx_np is not None else 0))
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
 
     # DRAM traffic per launch and warp instructions per coordinate step from the committed
@@ -549,7 +563,7 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
         # ~10 s of CPU work per config on a 16-thread host (config 0 is the whole config)
-        max_solves = {0: 256, 1: 1 << 20, 2: a.cpu_sample * 16, 3: 32768, 4: 8192}[a.config]
+        max_solves = {0: 256, 1: 1 << 20, 2: a.cpu_sample * 16, 3: 32768, 4: 8192}[a.config] // len(cfgs)
         Xh, Yh, Lh = wl.cpu_sample(a.warmup, max_solves)
         from oracle import oracle as O
 
@@ -558,19 +572,22 @@ def main():
         if a.dtype == "f32":
             Xh, Yh, Lh = Xh.astype(np.float32), Yh.astype(np.float32), np.asarray(Lh, dtype=np.float32)
         t0 = time.perf_counter()
-        ro = O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=wl.variant)
+        ros = [O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=v) for v in wl.variants]
         dt = time.perf_counter() - t0
         nsol = Xh.shape[0]
-        cpu = {"value": nsol / dt, "unit": "solves/s", "cores": nth, "kind": "port",
-               "sample": f"first {nsol} solves of the first timed step, CPU oracle (C restatement of "
-                         f"solve_locus{', binary32 build' if a.dtype == 'f32' else ''}) on {nth} threads, {dt:.1f} s"}
-        g = results[0]
-        gb = g.beta[:nsol].cpu().numpy()
-        go = g.objective[:nsol].cpu().numpy()
-        gs = g.steps[:nsol].cpu().numpy()
-        exact = int(np.sum(np.all(gb == ro["beta"], axis=1) & (go == ro["objective"]) & (gs == ro["steps"])))
-        rel = np.abs(go - ro["objective"]) / np.abs(ro["objective"])
-        parity = {"sample": nsol, "bit_exact": exact, "obj_within_1e-9": int(np.sum(rel <= 1e-9))}
+        cpu = {"value": nsol * len(ros) / dt, "unit": "solves/s", "cores": nth, "kind": "port",
+               "sample": f"first {nsol} solves of the first timed step x {'+'.join(wl.variants)}, CPU oracle "
+                         f"(C restatement of solve_locus{', binary32 build' if a.dtype == 'f32' else ''}) on "
+                         f"{nth} threads, {dt:.1f} s"}
+        exact = within = 0
+        for g, ro in zip(results[:len(ros)], ros):  # the first timed step's launch per variant
+            gb = g.beta[:nsol].cpu().numpy()
+            go = g.objective[:nsol].cpu().numpy()
+            gs = g.steps[:nsol].cpu().numpy()
+            exact += int(np.sum(np.all(gb == ro["beta"], axis=1) & (go == ro["objective"]) & (gs == ro["steps"])))
+            rel = np.abs(go - ro["objective"]) / np.abs(ro["objective"])
+            within += int(np.sum(rel <= 1e-9))
+        parity = {"sample": nsol * len(ros), "bit_exact": exact, "obj_within_1e-9": within}
 
     if rank == 0:
         line = {
@@ -581,7 +598,7 @@ def main():
             "scaling": "weak" if a.config != 3 else "strong", "vs_baseline": None, "dtype": a.dtype,
             "data": "synthetic (device Philox generator with the BASELINE config distributions)",
             "config": {"workload": f"config{a.config}", "description": wl.desc, "n": wl.n, "p": wl.p,
-                       "solves_per_step_per_gpu": solves_per_step, "variant": wl.variant,
+                       "solves_per_step_per_gpu": solves_per_step, "variant": "+".join(wl.variants),
                        "parallelism": f"shard{world} (independent problems, no collective)",
                        "kernel": "thread-per-problem sm_100a" if a.config == 1 else "warp-per-problem sm_100a",
                        "l2": "flushed between steps (256 MiB memset)"},
