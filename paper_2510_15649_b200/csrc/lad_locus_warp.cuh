@@ -58,7 +58,6 @@ struct WarpShared {
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
     int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
-    int cand2[PMAX];     // per axis: the one before (the median often alternates between two elements)
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
 };
@@ -479,10 +478,7 @@ __device__ __forceinline__ T median_by_order(WarpShared<PMAX, T> *W, int lane, u
     const T tk1 = shfl_t(key, ks + 1 < 32 ? ks + 1 : 31);
     t_new = tie ? dmul(T(0.5), dadd(tk, tk1)) : tk;
     if (cacheable) {  // identical values from every lane
-        const int mnew = __shfl_sync(FULLMASK, idx, ks);
-        W->cand2[j] = W->cand[j];
-        __syncwarp();
-        W->cand[j] = mnew;
+        W->cand[j] = __shfl_sync(FULLMASK, idx, ks);
     }
     return t_new;
 }
@@ -523,69 +519,67 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
         const unsigned q = W->wq[j][lane];
         const unsigned hq = W->halfq[j];
         const int m1 = W->cand[j];
-        // Where is element m relative to the median?  0: m is the median; +1: the
-        // median comes after m, -1: before m (decided beyond the margin); 2:
-        // undecided.  Exact integer sums: the answer is warp-uniform.  `below`
-        // returns this lane's position relative to m for the neighbour search.
-        auto test = [&](int m, T &lm, bool &below) {
-            lm = shfl_t(loc, m);
-            below = (loc < lm) | ((loc == lm) & (lane < m));
-            const unsigned qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
-            const unsigned qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
+        // Where is element m relative to the median, given the fixed-point
+        // weight before it (qb) and through it (qi)?  0: m is the median; +1:
+        // the median comes after m, -1: before m (decided beyond the margin);
+        // 2: undecided.  Exact integer sums: the answer is warp-uniform.
+        auto verdict = [&](unsigned qb, unsigned qi) {
             if ((qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q)) return 0;
             if (qi + MEDIAN_MARGIN_Q < hq) return 1;
             if (qb > hq + MEDIAN_MARGIN_Q) return -1;
             return 2;
         };
+        auto test = [&](int m, T &lm, bool &below, unsigned &qb, unsigned &qi) {
+            lm = shfl_t(loc, m);
+            below = (loc < lm) | ((loc == lm) & (lane < m));
+            qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
+            qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
+            return verdict(qb, qi);
+        };
         bool below1;
-        const int v1 = test(m1, t_new, below1);
+        unsigned qb1, qi1;
+        const int v1 = test(m1, t_new, below1, qb1, qi1);
         hit = v1 == 0;
         if (!hit) {
-            const int m2 = W->cand2[j];
-            bool below2;
-            int v2 = 2;
-            T l2;
-            if (m2 != m1) {
-                v2 = test(m2, l2, below2);
-                if (v2 == 0) {
-                    hit = true;
-                    t_new = l2;
-                    W->cand2[j] = m1;  // identical value from every lane
-                    W->cand[j] = m2;
-                }
-            }
             // Walk from m1 towards the median through its neighbours in the
             // stable (location, index) order: after a miss the median has
             // usually moved by one element (config 2: 71% of first-candidate
-            // misses), and a hop (two REDUX minima, one test) costs far less
-            // than ordering all breakpoints; the walk ends at the median, at a
-            // margin case or at the end of the order (<= 31 hops).  A hop's
-            // candidate is accepted only by the same exact test, so the walk
-            // changes the cost of a step, never its result.  Same-box A/B
-            // against no walk: config 2 +8.4%, config 4 +2.5%.
-            if (!hit && (v1 == 1 || v1 == -1)) {
+            // misses; an earlier second-candidate test of the median before
+            // last is subsumed: same-box A/B +1.6% without it).  The neighbour nb of the current element is the
+            // min/max (location, index) key on its side (two REDUX minima),
+            // and since nb is adjacent in the order its fixed-point sums follow
+            // exactly from the current ones: walking up, qb(nb) = qi(cur) and
+            // qi(nb) = qi(cur) + q(nb); walking down, qi(nb) = qb(cur) and
+            // qb(nb) = qb(cur) - q(nb).  The walk ends at the median, at a
+            // margin case or at the end of the order (<= 31 hops), and a hop's
+            // candidate is accepted by the same verdict as the candidates', so
+            // the walk changes the cost of a step, never its result.
+            if (v1 == 1 || v1 == -1) {
                 const OrderKey<T> key(loc);
-                int cur = m1;
-                bool below_cur = below1;
+                const bool up = v1 > 0;
+                bool side = up ? !(below1 | (lane == m1)) : below1;
+                unsigned qb = qb1, qi = qi1;
 #pragma unroll 1
                 for (int hop = 0; hop < 31; ++hop) {
-                    const bool side = v1 > 0 ? !(below_cur | (lane == cur)) : below_cur;
-                    const int nb = key.nearest(side, v1 > 0);
+                    const int nb = key.nearest(side, up);
                     if (nb < 0) break;
-                    bool below_nb;
-                    T lnb;
-                    const int vn = (nb == m2) ? v2 : test(nb, lnb, below_nb);
-                    if (vn == 0) {  // (m2 itself was tested above)
+                    const unsigned qn = __shfl_sync(FULLMASK, q, nb);
+                    if (up) {
+                        qb = qi;
+                        qi += qn;
+                    } else {
+                        qi = qb;
+                        qb -= qn;
+                    }
+                    const int vn = verdict(qb, qi);
+                    if (vn == 0) {
                         hit = true;
-                        t_new = lnb;
-                        W->cand2[j] = m1;
-                        W->cand[j] = nb;
+                        t_new = shfl_t(loc, nb);
+                        W->cand[j] = nb;  // identical value from every lane
                         break;
                     }
-                    if (vn != v1) break;  // undecided, or the median lies between cur and nb
-                    if (nb == m2) below_nb = below2;
-                    cur = nb;
-                    below_cur = below_nb;
+                    if (vn != v1) break;  // undecided
+                    side = side & (lane != nb);
                 }
             }
         }
@@ -802,7 +796,6 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, LAD_WARP_MIN_BLOCKS) loc
     uint32_t perm_valid = 0;
     Ctl<PMAX> &C = W->C;
     if (lane < PMAX) W->cand[lane] = 0;
-    if (lane < PMAX) W->cand2[lane] = 1;
     if (lane == 0) C.pc = PC_FETCH;
     __syncwarp();
     for (;;) {
