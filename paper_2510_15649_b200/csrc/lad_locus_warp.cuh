@@ -517,7 +517,7 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     bool hit = false;
     if (cacheable) {
         const unsigned q = W->wq[j][lane];
-        const unsigned hq = W->halfq[j];
+        const unsigned hq = __reduce_max_sync(FULLMASK, W->halfq[j]);  // uniform register
         const int m1 = W->cand[j];
         // Where is element m relative to the median, given the fixed-point
         // weight before it (qb) and through it (qi)?  0: m is the median; +1:
@@ -529,31 +529,28 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
             if (qb > hq + MEDIAN_MARGIN_Q) return -1;
             return 2;
         };
-        auto test = [&](int m, T &lm, bool &below, unsigned &qb, unsigned &qi) {
-            lm = shfl_t(loc, m);
-            below = (loc < lm) | ((loc == lm) & (lane < m));
-            qb = __reduce_add_sync(FULLMASK, below ? q : 0u);
-            qi = __reduce_add_sync(FULLMASK, (below | (lane == m)) ? q : 0u);
-            return verdict(qb, qi);
-        };
-        bool below1;
-        unsigned qb1, qi1;
-        const int v1 = test(m1, t_new, below1, qb1, qi1);
-        hit = v1 == 0;
+        // first candidate (the hit path: ~85% of steps decide here)
+        t_new = shfl_t(loc, m1);
+        const bool below1 = (loc < t_new) | ((loc == t_new) & (lane < m1));
+        const unsigned qb1 = __reduce_add_sync(FULLMASK, below1 ? q : 0u);
+        const unsigned qi1 = __reduce_add_sync(FULLMASK, (below1 | (lane == m1)) ? q : 0u);
+        hit = (qb1 + MEDIAN_MARGIN_Q < hq) & (qi1 > hq + MEDIAN_MARGIN_Q);
         if (!hit) {
+            const int v1 = verdict(qb1, qi1);
             // Walk from m1 towards the median through its neighbours in the
             // stable (location, index) order: after a miss the median has
             // usually moved by one element (config 2: 71% of first-candidate
-            // misses; an earlier second-candidate test of the median before
-            // last is subsumed: same-box A/B +1.6% without it).  The neighbour nb of the current element is the
-            // min/max (location, index) key on its side (two REDUX minima),
-            // and since nb is adjacent in the order its fixed-point sums follow
-            // exactly from the current ones: walking up, qb(nb) = qi(cur) and
-            // qi(nb) = qi(cur) + q(nb); walking down, qi(nb) = qb(cur) and
-            // qb(nb) = qb(cur) - q(nb).  The walk ends at the median, at a
-            // margin case or at the end of the order (<= 31 hops), and a hop's
-            // candidate is accepted by the same verdict as the candidates', so
-            // the walk changes the cost of a step, never its result.
+            // misses; the walk also subsumes an earlier test of the median
+            // before last: same-box A/B +1.6% without it).  The neighbour nb
+            // of the current element is the min/max (location, index) key on
+            // its side (two REDUX minima), and since nb is adjacent in the
+            // order its fixed-point sums follow exactly from the current ones:
+            // walking up, qb(nb) = qi(cur) and qi(nb) = qi(cur) + q(nb);
+            // walking down, qi(nb) = qb(cur) and qb(nb) = qb(cur) - q(nb).
+            // The walk ends at the median, at a margin case or at the end of
+            // the order (<= 31 hops), and a hop's candidate is accepted by the
+            // same verdict as the first's, so the walk changes the cost of a
+            // step, never its result.
             if (v1 == 1 || v1 == -1) {
                 const OrderKey<T> key(loc);
                 const bool up = v1 > 0;
