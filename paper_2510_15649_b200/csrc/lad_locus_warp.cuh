@@ -56,6 +56,7 @@ struct WarpShared {
     T B[PMAX];       // beta of the running descent (warp-uniform)
     T sa[32], sw[32], sz[32];
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
+    T2 sl[2];        // ddot lane-tree partial sums (S0, S1), (S2, S3)
     int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
@@ -597,31 +598,35 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     const T wv = in ? w : T(0);
     const int n1 = cnt & -16;
     const T pr = dmul(a, wv);
-    T dot = T(0);
+    // The four 256-bit lane sums S_0..S_3 come from shuffles into lanes 0..3
+    // and go through shared memory, where every lane folds (S0 + S2) + (S1 + S3)
+    // itself (one store/load instead of three dependent shuffle rounds).
+    T *const sl = reinterpret_cast<T *>(W->sl);
     if (n1 == 16) {
         const T q4 = shfl_down_t(pr, 4), q8 = shfl_down_t(pr, 8), q12 = shfl_down_t(pr, 12);
         const T S = dadd(dadd(dadd(pr, q4), q8), q12);
-        const T u = dadd(S, shfl_down_t(S, 2));
-        dot = shfl_t(dadd(u, shfl_down_t(u, 1)), 0);
+        if (lane < 4) sl[lane] = S;
     } else if (n1 == 32) {
         const T A2 = dadd(pr, shfl_down_t(pr, 4));
         const T a8 = shfl_down_t(A2, 8), a16 = shfl_down_t(A2, 16), a24 = shfl_down_t(A2, 24);
         const T S = dadd(dadd(dadd(A2, a8), a16), a24);
-        const T u = dadd(S, shfl_down_t(S, 2));
-        dot = shfl_t(dadd(u, shfl_down_t(u, 1)), 0);
+        if (lane < 4) sl[lane] = S;
     }
-    if (n1 < cnt) {  // FMA tail in index order, operands as (a, w) pairs from shared memory
-        W->aw[lane] = {a, wv};
-        __syncwarp();
+    W->aw[lane] = {a, wv};  // FMA tail operands as (a, w) pairs
+    __syncwarp();
+    T dot = T(0);
+    if (n1 > 0) {
+        const auto s01 = W->sl[0], s23 = W->sl[1];
+        dot = dadd(dadd(s01.x, s23.x), dadd(s01.y, s23.y));
+    }
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {  // tail length cnt - n1 < 16
-            if (n1 + t < cnt) {
-                const auto q = W->aw[n1 + t];
-                dot = dfma(q.x, q.y, dot);
-            }
+    for (int t = 0; t < 16; ++t) {  // FMA tail in index order, length cnt - n1 < 16
+        if (n1 + t < cnt) {
+            const auto q = W->aw[n1 + t];
+            dot = dfma(q.x, q.y, dot);
         }
-        __syncwarp();
     }
+    __syncwarp();
     const T v_new = dadd(constant, dot);
     if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
         const T delta = dsub(t_new, bj);
