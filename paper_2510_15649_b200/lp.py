@@ -19,7 +19,8 @@ import numpy as np
 from . import _lib
 from .config import DEFAULT_LAMBDA_FLOOR
 from .errors import InvalidInputError, SimplexError
-from .solver import Coefficients, SolveResult, _check, _is_torch, _spec_arrays, _validate_device, _validate_host
+from .solver import (Coefficients, SolveResult, _check, _is_torch, _spec_arrays, _to_device, _validate_device,
+                     _validate_host)
 
 PIVOT_RULES = ("bland", "dantzig_with_bland_fallback")
 
@@ -127,7 +128,7 @@ def solve_lp_batched(X, y, lam, cfg: SimplexConfig | None = None, *, lambda_floo
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (_to_device(a, dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device

@@ -30,6 +30,19 @@ STATUS_UNBOUNDED = 1
 STATUS_INVALID = 2
 
 
+def _to_device(a, dev):
+    """Host array -> device tensor without a host-side copy (pinned caller buffers then copy
+    by DMA).  torch.from_numpy warns on read-only arrays (the reference's frozen datasets);
+    the tensor is only read by the copy, so the warning is suppressed instead of copying."""
+    import warnings
+
+    import torch
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
 def _is_torch(a) -> bool:
     try:
         import torch
@@ -207,7 +220,7 @@ def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=N
     if host:
         X, y, lam = _validate_host(X, y, lam, f32)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (_to_device(a, dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam, None, f32)
         dev = Xt.device
@@ -256,7 +269,7 @@ def solve_brute_batched(X, y, lam, max_variables: int = 6, max_candidates: int =
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (_to_device(a, dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
@@ -300,8 +313,8 @@ def evaluate_objective_batched(X, y, lam, beta, *, lambda_floor: float = DEFAULT
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
-        bt = torch.from_numpy(np.array(beta, dtype=np.float64, order="C")).to(dev)
+        Xt, yt, lt = (_to_device(a, dev) for a in (X, y, lam))
+        bt = _to_device(np.asarray(beta, dtype=np.float64), dev)
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
@@ -325,7 +338,7 @@ def axiswise_minimum_batched(X, y, lam, beta, skip=None, tol: float = 1e-9, *,
     if host:
         X, y, lam = _validate_host(X, y, lam)
         dev = torch.device("cuda")
-        Xt, yt, lt = (torch.from_numpy(np.array(a)).to(dev) for a in (X, y, lam))
+        Xt, yt, lt = (_to_device(a, dev) for a in (X, y, lam))
     else:
         Xt, yt, lt = _validate_device(X, y, lam)
         dev = Xt.device
