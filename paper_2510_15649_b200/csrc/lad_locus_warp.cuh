@@ -8,8 +8,8 @@
 //   * weighted median: test the axis' last median element (then the one
 //     before it, then its neighbours in order) with two exact fixed-point
 //     warp sums against half the total weight, decided only beyond a margin;
-//     otherwise order all (location, index) pairs (cached permutation,
-//     odd-even repair or a 32-lane bitonic network) and scan the weights
+//     otherwise order all (location, index) pairs (a 32-lane bitonic
+//     network of shuffles) and scan the weights
 //     (FP32 Kogge-Stone with a margin, else numpy's exact sequential cumsum),
 //     so the result is always the reference's;
 //   * v_new: OpenBLAS ddot's summation tree mapped onto shuffles, the FMA tail
@@ -43,6 +43,8 @@ constexpr int WARPS_PER_BLOCK = LAD_WARP_WARPS_PER_BLOCK;
 // round-to-nearest whenever nothing under- or overflows: |r| and |x| within
 // 2^+-450 (binary64) or 2^+-50 (binary32).  Used where shared memory holds the
 // reciprocal table (binary32, or binary64 with p <= 5).
+// (For binary64 p = 8 the table costs more than it saves: 2 KB more shared
+// memory per warp, config 4 -13% in a same-box A/B.)
 template <int PMAX, typename T>
 constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5;
 
@@ -57,7 +59,6 @@ struct WarpShared {
     T sa[32], sw[32], sz[32];
     T2 aw[32];       // (|t - loc_i|, w_i) pairs for the ddot FMA tail
     T2 sl[2];        // ddot lane-tree partial sums (S0, S1), (S2, S3)
-    int perm[PMAX][32];  // per axis: sorted position -> element of the last sort
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
@@ -326,44 +327,6 @@ __device__ __forceinline__ void bitonic32m(T &key, int &idx, uint32_t inv_mask)
     }
 }
 
-// (key, idx) ascending across lanes 0..31 (lexicographic)?
-template <typename T>
-__device__ __forceinline__ bool warp_is_sorted(T key, int idx, int lane)
-{
-    const T nk = shfl_down_t(key, 1);
-    const int ni = __shfl_down_sync(FULLMASK, idx, 1);
-    const bool ok = (lane == 31) || (key < nk) || ((key == nk) && (idx < ni));
-    return __all_sync(FULLMASK, ok);
-}
-
-// number of adjacent (key, idx) pairs out of ascending order
-template <typename T>
-__device__ __forceinline__ int warp_order_violations(T key, int idx, int lane)
-{
-    const T nk = shfl_down_t(key, 1);
-    const int ni = __shfl_down_sync(FULLMASK, idx, 1);
-    const bool ok = (lane == 31) || (key < nk) || ((key == nk) && (idx < ni));
-    return __popc(__ballot_sync(FULLMASK, !ok));
-}
-
-// One odd-even transposition phase: pairs (2i, 2i+1) for phase 0, (2i+1, 2i+2)
-// for phase 1; the lower lane of a pair keeps the smaller (key, idx).
-template <typename T>
-__device__ __forceinline__ void oddeven_phase(T &key, int &idx, int lane, int phase)
-{
-    const bool odd = lane & 1;
-    const bool lower = (phase == 0) ? !odd : odd;
-    int partner = lower ? lane + 1 : lane - 1;
-    const bool paired = partner >= 0 && partner < 32;
-    partner = paired ? partner : lane;
-    const T pk = shfl_t(key, partner);
-    const int pi = __shfl_sync(FULLMASK, idx, partner);
-    const bool plt = (pk < key) | ((pk == key) & (pi < idx));
-    const bool take = paired && (lower ? plt : !plt);
-    key = take ? pk : key;
-    idx = take ? pi : idx;
-}
-
 // numpy's sequential cumsum in sorted order, recomputed exactly (rare path:
 // only when the parallel scan leaves a comparison within its error margin).
 template <typename T>
@@ -410,43 +373,18 @@ __device__ __forceinline__ void sparse_column(WarpShared<PMAX, T> *W, int lane, 
     cnt = k + 1;
 }
 
-// Weighted median by ordering (the fast path's miss): stable order of (location,
-// index) -- cached permutation, odd-even repair, bitonic network -- then the
-// cumulative-weight decision.
+// Weighted median by ordering (the walk's rare miss: a margin case, the first
+// step of an axis, or a sparse column): stable order of (location, index) by
+// the 32-lane bitonic network, then the cumulative-weight decision.
 template <int PMAX, int CNTC, typename T>
 __device__ __forceinline__ T median_by_order(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j,
-                                             bool cacheable, int cnt_rt, T loc, T w, uint32_t &perm_valid)
+                                             bool cacheable, int cnt_rt, T loc, T w)
 {
     const int cnt = CNTC > 0 ? CNTC : cnt_rt;
     T t_new;
-    // stable order by (location, index).  The order is unique, so if this
-    // axis' permutation from its previous evaluation is still sorted under the
-    // new locations it is the answer; otherwise odd-even transposition rounds
-    // repair a nearly sorted permutation, and the 15-stage network runs last.
-    T key;
-    int idx;
-    bool sorted = false;
-    if (cacheable && ((perm_valid >> j) & 1u)) {
-        idx = W->perm[j][lane];
-        key = shfl_t(loc, idx);
-        const int violations = warp_order_violations(key, idx, lane);
-        sorted = violations == 0;
-        // a few adjacent inversions: odd-even rounds; many: straight to the network
-#pragma unroll 1
-        for (int round = 0; round < 2 && !sorted && violations <= 6; ++round) {
-            oddeven_phase(key, idx, lane, 0);
-            oddeven_phase(key, idx, lane, 1);
-            sorted = warp_is_sorted(key, idx, lane);
-        }
-        if (sorted) W->perm[j][lane] = idx;
-    }
-    if (!sorted) {
-        key = loc;
-        idx = lane;
-        bitonic32m(key, idx, inv_mask);
-        if (cacheable) W->perm[j][lane] = idx;
-    }
-    if (cacheable) perm_valid |= 1u << j;
+    T key = loc;
+    int idx = lane;
+    bitonic32m(key, idx, inv_mask);
     const T ws = shfl_t(w, idx);
     // Cumulative weights only *locate* k = first cum >= total/2.  An FP32
     // Kogge-Stone scan differs from the sequential cumsum in T by at most
@@ -489,9 +427,9 @@ __device__ __forceinline__ T median_by_order(WarpShared<PMAX, T> *W, int lane, u
 // (config 2: +5%).  For p = 8 misses are frequent enough that the call costs more.
 template <int PMAX, int CNTC, typename T>
 __device__ __noinline__ T median_by_order_call(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j,
-                                               bool cacheable, int cnt_rt, T loc, T w, uint32_t &perm_valid)
+                                               bool cacheable, int cnt_rt, T loc, T w)
 {
-    return median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
+    return median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w);
 }
 
 // Weighted median, skip test, v_new and strict accept of one coordinate step
@@ -501,8 +439,7 @@ __device__ __noinline__ T median_by_order_call(WarpShared<PMAX, T> *W, int lane,
 template <int PMAX, int CNTC, typename T>
 __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, int j, T lam,
                                               bool cacheable, int cnt_rt, T loc, T w, T zsum, bool have_zero,
-                                              bool row, T xij, T bj, T &r, T &f_cur, T &sum_abs_b,
-                                              uint32_t &perm_valid)
+                                              bool row, T xij, T bj, T &r, T &f_cur, T &sum_abs_b)
 {
     const int cnt = CNTC > 0 ? CNTC : cnt_rt;
     // Fast path (dense columns): the weighted median is usually the same
@@ -584,9 +521,9 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     }
     if (!hit) {
         if constexpr (PMAX <= 5)
-            t_new = median_by_order_call<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
+            t_new = median_by_order_call<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w);
         else
-            t_new = median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w, perm_valid);
+            t_new = median_by_order<PMAX, CNTC, T>(W, lane, inv_mask, j, cacheable, cnt_rt, loc, w);
     }
     if (fabs(dsub(t_new, bj)) <= dmul(T(1e-14), dadd(T(1), fabs(bj)))) return;  // ccd.py:172
     T constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
@@ -652,9 +589,8 @@ __device__ __noinline__ StepState<T> sparse_step(WarpShared<PMAX, T> *W, int lan
     T loc, w, zsum;
     int cnt;
     sparse_column<PMAX, T>(W, lane, n, st.r, xij, bj, lam, loc, w, cnt, zsum);
-    uint32_t unused = 0;  // sparse columns never use the order cache
     median_update<PMAX, 0, T>(W, lane, inv_mask, j, lam, false, cnt, loc, w, zsum, true, row, xij, bj, st.r, st.f_cur,
-                              st.sum_abs_b, unused);
+                              st.sum_abs_b);
     return st;
 }
 
@@ -663,7 +599,7 @@ __device__ __noinline__ StepState<T> sparse_step(WarpShared<PMAX, T> *W, int lan
 template <int PMAX, int NC, typename T>
 __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint32_t inv_mask, const T *xrow,
                                           const T *yrow, int n_rt, int j, T lam, bool col_sparse, T &r, T &f_cur,
-                                          T &sum_abs_b, uint32_t &perm_valid)
+                                          T &sum_abs_b)
 {
     const T INF = inf_of<T>();
     const int n = NC > 0 ? NC : n_rt;
@@ -683,7 +619,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
         const T loc = row ? dadd(q, bj) : (lane == n ? T(0) : INF);
         const T w = row ? fabs(xij) : (lane == n ? lam : T(0));
         median_update<PMAX, (NC > 0 ? NC + 1 : 0), T>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, T(0), false,
-                                                      row, xij, bj, r, f_cur, sum_abs_b, perm_valid);
+                                                      row, xij, bj, r, f_cur, sum_abs_b);
     } else if constexpr (PMAX <= 5) {
         const StepState<T> st = sparse_step<PMAX, T>(W, lane, inv_mask, n, j, lam, row, xij, bj, {r, f_cur, sum_abs_b});
         r = st.r;
@@ -694,7 +630,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
         int cnt;
         sparse_column<PMAX, T>(W, lane, n, r, xij, bj, lam, loc, w, cnt, zsum);
         median_update<PMAX, 0, T>(W, lane, inv_mask, j, lam, false, cnt, loc, w, zsum, true, row, xij, bj, r, f_cur,
-                                  sum_abs_b, perm_valid);
+                                  sum_abs_b);
     }
 }
 
@@ -714,11 +650,10 @@ __device__ __forceinline__ T warp_objective(WarpShared<PMAX, T> *W, int lane, in
 // ccd_descend (ccd.py:126-206) for the descent request in C, all lanes.
 template <int PMAX, int NC, typename T>
 __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
-                                          int p_rt, uint32_t &perm_valid_io)
+                                          int p_rt)
 {
     const int n = NC > 0 ? NC : n_rt;
     const int p = NC > 0 ? PMAX : p_rt;
-    uint32_t perm_valid = perm_valid_io;  // register copy for the step loop
     const int frozen = C.req_frozen;
     const double tol = C.req_tol;
     const int max_sweeps = C.req_sweeps;
@@ -744,7 +679,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
     } else {
         for (;;) {
             warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, j, lam, (sparse >> j) & 1u, r, f_cur,
-                                   sum_abs_b, perm_valid);
+                                   sum_abs_b);
             ++steps;
             int jn = j + 1;
             jn += (jn == frozen);
@@ -763,7 +698,6 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
             j = j0;
         }
     }
-    perm_valid_io = perm_valid;
     __syncwarp();
     const T obj = warp_objective<PMAX, T>(W, lane, n, p, lam);
     const int D = C.D;
@@ -785,7 +719,8 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
 template <int PMAX, int NC, typename T>
 __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, LAD_WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
 {
-    __shared__ WarpShared<PMAX, T> WS[WARPS_PER_BLOCK];
+    extern __shared__ __align__(16) unsigned char warp_smem[];  // WARPS_PER_BLOCK x WarpShared
+    WarpShared<PMAX, T> *WS = reinterpret_cast<WarpShared<PMAX, T> *>(warp_smem);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     WarpShared<PMAX, T> *W = &WS[wib];
@@ -793,9 +728,6 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, LAD_WARP_MIN_BLOCKS) loc
     const int slot = blockIdx.x * WARPS_PER_BLOCK + wib;
     WarpAccess<PMAX, T> acc{n, p, lane, W};
     const uint32_t inv_mask = bitonic_inv_mask(lane);
-    // cached breakpoint orders per axis (validated before every use, so they
-    // may be carried across descents and problems)
-    uint32_t perm_valid = 0;
     Ctl<PMAX> &C = W->C;
     if (lane < PMAX) W->cand[lane] = 0;
     if (lane == 0) C.pc = PC_FETCH;
@@ -804,7 +736,7 @@ __global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, LAD_WARP_MIN_BLOCKS) loc
         int act = controller<PMAX>(C, A, acc, slot);
         __syncwarp();
         if (act == ACT_EXIT) break;
-        warp_descent<PMAX, NC, T>(W, C, lane, inv_mask, n, p, perm_valid);
+        warp_descent<PMAX, NC, T>(W, C, lane, inv_mask, n, p);
     }
 }
 
