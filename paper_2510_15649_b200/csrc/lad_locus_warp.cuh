@@ -530,9 +530,11 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     if (have_zero) constant = dadd(constant, zsum);
     // v_new = constant + |t - loc| @ weights in OpenBLAS ddot's order: n&-16
     // products folded by the SkylakeX lane tree (shuffles), then the FMA tail.
-    const bool in = lane < cnt;
-    const T a = in ? fabs(dsub(t_new, loc)) : T(0);
-    const T wv = in ? w : T(0);
+    // Lanes >= cnt (pads) never enter the sum: the lane tree reads lanes 0..15
+    // only when cnt >= 16 (lanes 0..31 when cnt = 32) and the tail reads
+    // elements < cnt, so their (a, w) need no zeroing.
+    const T a = fabs(dsub(t_new, loc));
+    const T wv = w;
     const int n1 = cnt & -16;
     const T pr = dmul(a, wv);
     // The four 256-bit lane sums S_0..S_3 come from shuffles into lanes 0..3
