@@ -29,13 +29,19 @@
 namespace lad {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
-#ifndef LAD_WARP_WARPS_PER_BLOCK
-#define LAD_WARP_WARPS_PER_BLOCK 7  // 7 warps x 4 blocks: 72 registers, 178 KB shared per SM
+// Launch shape, 4 blocks per SM: p <= 5 runs 8 warps per block (32 warps/SM,
+// 64 registers), p = 8 runs 7 (28 warps/SM, 72 registers).  Same-box A/B: 32
+// warps are +3% for config 2 and -2.5% for config 4 (whose longer step body
+// spills less at 72 registers).
+#ifndef LAD_WARP_WARPS_NARROW
+#define LAD_WARP_WARPS_NARROW 8
 #endif
-#ifndef LAD_WARP_MIN_BLOCKS
-#define LAD_WARP_MIN_BLOCKS 4
+#ifndef LAD_WARP_WARPS_WIDE
+#define LAD_WARP_WARPS_WIDE 7
 #endif
-constexpr int WARPS_PER_BLOCK = LAD_WARP_WARPS_PER_BLOCK;
+constexpr int WARP_MIN_BLOCKS = 4;
+template <int PMAX>
+constexpr int warps_per_block = PMAX <= 5 ? LAD_WARP_WARPS_NARROW : LAD_WARP_WARPS_WIDE;
 
 // Division by a precomputed reciprocal: q = RN(r * y), then two corrections
 // q += RN(r - q * x) * y with y = RN(1 / x).  The first makes q faithful, the
@@ -719,15 +725,15 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
 
 // PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
 template <int PMAX, int NC, typename T>
-__global__ void __launch_bounds__(32 * WARPS_PER_BLOCK, LAD_WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32 * warps_per_block<PMAX>, WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
 {
-    extern __shared__ __align__(16) unsigned char warp_smem[];  // WARPS_PER_BLOCK x WarpShared
+    extern __shared__ __align__(16) unsigned char warp_smem[];  // warps_per_block x WarpShared
     WarpShared<PMAX, T> *WS = reinterpret_cast<WarpShared<PMAX, T> *>(warp_smem);
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     WarpShared<PMAX, T> *W = &WS[wib];
     const int n = NC > 0 ? NC : A.n, p = NC > 0 ? PMAX : A.p;
-    const int slot = blockIdx.x * WARPS_PER_BLOCK + wib;
+    const int slot = blockIdx.x * warps_per_block<PMAX> + wib;
     WarpAccess<PMAX, T> acc{n, p, lane, W};
     const uint32_t inv_mask = bitonic_inv_mask(lane);
     Ctl<PMAX> &C = W->C;

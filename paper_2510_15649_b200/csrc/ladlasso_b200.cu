@@ -86,8 +86,8 @@ Variant make_thread_variant()
 template <int P, int NC, typename T = double>
 Variant make_warp_variant()
 {
-    return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, sizeof(lad::WarpShared<P, T>) * lad::WARPS_PER_BLOCK,
-                   32 * lad::WARPS_PER_BLOCK, lad::WARPS_PER_BLOCK};
+    constexpr int wpb = lad::warps_per_block<P>;
+    return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, sizeof(lad::WarpShared<P, T>) * wpb, 32 * wpb, wpb};
 }
 
 int g_kernel_policy = LAD_KERNEL_AUTO;
