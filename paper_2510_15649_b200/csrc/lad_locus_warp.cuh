@@ -32,14 +32,17 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 // Launch shape, 4 blocks per SM: p <= 5 runs 8 warps per block (32 warps/SM,
 // 64 registers), p = 8 runs 7 (28 warps/SM, 72 registers).  Same-box A/B: 32
 // warps are +3% for config 2 and -2.5% for config 4 (whose longer step body
-// spills less at 72 registers).
+// spills less at 72 registers); 36 warps at 56 registers: -3% for config 2.
 #ifndef LAD_WARP_WARPS_NARROW
 #define LAD_WARP_WARPS_NARROW 8
 #endif
 #ifndef LAD_WARP_WARPS_WIDE
 #define LAD_WARP_WARPS_WIDE 7
 #endif
-constexpr int WARP_MIN_BLOCKS = 4;
+#ifndef LAD_WARP_MIN_BLOCKS
+#define LAD_WARP_MIN_BLOCKS 4
+#endif
+constexpr int WARP_MIN_BLOCKS = LAD_WARP_MIN_BLOCKS;
 template <int PMAX>
 constexpr int warps_per_block = PMAX <= 5 ? LAD_WARP_WARPS_NARROW : LAD_WARP_WARPS_WIDE;
 
