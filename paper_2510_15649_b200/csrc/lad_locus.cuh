@@ -1021,8 +1021,19 @@ __host__ __device__ constexpr size_t smem_doubles_per_warp()
     return (size_t)NMAX * PMAX * 32 + (size_t)NMAX * 32 + (size_t)(NMAX + 1) * 32;
 }
 
+// Occupancy hint for the compile-time-shape kernel (config 1: n = 10, p = 2):
+// 18 one-warp blocks per SM caps it at 96 registers (21 resident warps instead
+// of 16 at 128).  The per-thread controller state lives in local memory and
+// misses L1 either way; more warps in flight hide more of it.  Same-box A/B:
+// +15.6% (hints 12 / 17 / 19 / 20 / 24: -1% / +14% / +14% / +13% / -1%).
+#ifndef LAD_THREAD_MIN_BLOCKS
+#define LAD_THREAD_MIN_BLOCKS 18
+#endif
+template <int NMAX, bool EXACT>
+constexpr int thread_min_blocks = (EXACT && NMAX <= 10) ? LAD_THREAD_MIN_BLOCKS : 1;
+
 template <int NMAX, int PMAX, bool EXACT>
-__global__ void __launch_bounds__(32) locus_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kernel(LocusArgs A)
 {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
