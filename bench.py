@@ -520,10 +520,9 @@ def main():
         hidx = torch.empty(wl.data_index.shape, dtype=torch.int64, pin_memory=True)
         hidx.copy_(wl.data_index)
         hidx_np = hidx.numpy()
-    m_warm = min(1024, host[0][2].shape[0])  # untimed warm-up of the host-buffer path (allocator, first call)
-    lad.solve_locus_batched(host[0][0][: m_warm if hidx_np is None else host[0][0].shape[0]],
-                            host[0][1][: m_warm if hidx_np is None else host[0][1].shape[0]], host[0][2][:m_warm],
-                            cfgs[0], data_index=None if hidx_np is None else hidx_np[:m_warm])
+    # untimed warm-up of the host-buffer path at full size (the device memory pool grows to the
+    # step's buffers once; the device-side arm likewise runs its warm-up steps untimed)
+    lad.solve_locus_batched(host[0][0], host[0][1], host[0][2], cfgs[0], data_index=hidx_np)
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
