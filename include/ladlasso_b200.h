@@ -185,6 +185,12 @@ int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, int64_t B, in
 int lad_subsets_f64(const double *X0, const double *Y0, int32_t n0, int32_t p, int32_t keep, int64_t first, int64_t B,
                     double *X, double *Y, void *stream);
 
+/* Host -> device copy of `bytes` from a caller's host buffer, ordered on `stream`
+ * (cudaMemcpyAsync on the raw pointer: DMA when the buffer is page-locked, driver
+ * staging otherwise).  Used by the Python host-buffer paths of the batched calls
+ * that have no _host entry point (brute force, simplex, descents, certificates). */
+int lad_copy_h2d(void *dst, const void *src, size_t bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,7 @@ SYMBOLS = (
     "lad_version",
     "lad_last_error",
     "lad_kernel_launches",
+    "lad_copy_h2d",
     "lad_default_params",
     "lad_set_kernel_policy",
     "lad_set_axis_parallel",
@@ -131,6 +132,7 @@ def load(build_if_missing: bool = False):
                                    i32, vp]
     L.lad_generate_f64.argtypes = [i32, C.c_uint64, i64, i64, i32, i32, vp, vp, vp, vp, vp]
     L.lad_subsets_f64.argtypes = [vp, vp, i32, i32, i32, i64, i64, vp, vp, vp]
+    L.lad_copy_h2d.argtypes = [vp, vp, C.c_size_t, vp]
     L.lad_kernel_launches.restype = C.c_longlong
     for name in SYMBOLS:
         if name not in ("lad_version", "lad_last_error", "lad_kernel_launches", "lad_default_params"):

@@ -22,7 +22,7 @@
 #include "lad_locus_warp.cuh"
 #include "lad_locus_block.cuh"
 
-#define LAD_VERSION 102
+#define LAD_VERSION 103
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};  // kernels this library has launched (all threads)
@@ -275,6 +275,14 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
 }
 
 }  // namespace
+
+extern "C" int lad_copy_h2d(void *dst, const void *src, size_t bytes, void *stream)
+{
+    if (bytes == 0) return LAD_OK;
+    if (dst == nullptr || src == nullptr) return fail(LAD_E_INVALID, "lad_copy_h2d: null pointer");
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    return LAD_OK;
+}
 
 extern "C" int lad_set_axis_parallel(int32_t enable)
 {

@@ -19,8 +19,8 @@ import numpy as np
 from . import _lib
 from .config import DEFAULT_LAMBDA_FLOOR
 from .errors import InvalidInputError, SimplexError
-from .solver import (Coefficients, SolveResult, _check, _is_torch, _spec_arrays, _to_device, _validate_device,
-                     _validate_host)
+from .solver import (Coefficients, SolveResult, _check, _is_torch, _spec_arrays, _to_device, _to_host,
+                     _validate_device, _validate_host)
 
 PIVOT_RULES = ("bland", "dantzig_with_bland_fallback")
 
@@ -151,7 +151,7 @@ def solve_lp_batched(X, y, lam, cfg: SimplexConfig | None = None, *, lambda_floo
                               int(trace_cap), torch.cuda.current_stream(dev).cuda_stream))
     out = LpBatch(beta, obj, piv, cv.bool(), st, xf, bs, tr)
     if host:
-        out = LpBatch(*[None if v is None else v.cpu().numpy() for v in
+        out = LpBatch(*[None if v is None else _to_host(v) for v in
                         (beta, obj, piv, cv.bool(), st, xf, bs, tr)])
     return out
 

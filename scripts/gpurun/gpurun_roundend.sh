@@ -7,6 +7,6 @@ for v in ternary quadrature; do python bench.py --variant $v --steps 3 --no-cpu 
 for c in 0 1 3 4; do python bench.py --config $c --steps 3 --warmup 3 > gpurun_out/bench_config$c.json 2> gpurun_out/bench_config$c.err; echo "cfg$c rc=$?"; done
 python bench.py --config 4 --dtype f32 --steps 3 --warmup 3 > gpurun_out/bench_config4_f32.json 2> gpurun_out/bench_config4_f32.err; echo "cfg4 f32 rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --block 2048 --no-cpu > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"
-python bench.py --solver lp --steps 3 --warmup 2 > gpurun_out/bench_lp.json 2> gpurun_out/bench_lp.err; echo "lp rc=$?"
-python bench.py --solver brute --steps 3 --warmup 2 > gpurun_out/bench_brute.json 2> gpurun_out/bench_brute.err; echo "brute rc=$?"
+python bench.py --solver lp --steps 10 --warmup 3 > gpurun_out/bench_lp.json 2> gpurun_out/bench_lp.err; echo "lp rc=$?"
+python bench.py --solver brute --steps 10 --warmup 3 > gpurun_out/bench_brute.json 2> gpurun_out/bench_brute.err; echo "brute rc=$?"
 bash scripts/gpurun/gpurun_fullprof.sh
