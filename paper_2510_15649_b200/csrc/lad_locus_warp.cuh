@@ -29,10 +29,11 @@
 namespace lad {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
-// Launch shape, 4 blocks per SM: p <= 5 runs 8 warps per block (32 warps/SM,
-// 64 registers), p = 8 runs 7 (28 warps/SM, 72 registers).  Same-box A/B: 32
-// warps are +3% for config 2 and -2.5% for config 4 (whose longer step body
-// spills less at 72 registers); 36 warps at 56 registers: -3% for config 2.
+// Launch shape, 4 blocks per SM: 8 warps per block (32 warps/SM, 64 registers),
+// except binary64 p = 8 with 7 (28 warps/SM, 72 registers).  Same-box A/B: 32
+// warps are +3% for config 2, +3.4% for config 4 in fp32 and -2% for config 4
+// in fp64 (whose longer step body spills less at 72 registers); 36 warps at 56
+// registers: -3% for config 2.
 #ifndef LAD_WARP_WARPS_NARROW
 #define LAD_WARP_WARPS_NARROW 8
 #endif
@@ -43,8 +44,8 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 #define LAD_WARP_MIN_BLOCKS 4
 #endif
 constexpr int WARP_MIN_BLOCKS = LAD_WARP_MIN_BLOCKS;
-template <int PMAX>
-constexpr int warps_per_block = PMAX <= 5 ? LAD_WARP_WARPS_NARROW : LAD_WARP_WARPS_WIDE;
+template <int PMAX, typename T>
+constexpr int warps_per_block = (PMAX <= 5 || sizeof(T) == 4) ? LAD_WARP_WARPS_NARROW : LAD_WARP_WARPS_WIDE;
 
 // Division by a precomputed reciprocal: q = RN(r * y), then two corrections
 // q += RN(r - q * x) * y with y = RN(1 / x).  The first makes q faithful, the
@@ -728,7 +729,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
 
 // PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
 template <int PMAX, int NC, typename T>
-__global__ void __launch_bounds__(32 * warps_per_block<PMAX>, WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
 {
     extern __shared__ __align__(16) unsigned char warp_smem[];  // warps_per_block x WarpShared
     WarpShared<PMAX, T> *WS = reinterpret_cast<WarpShared<PMAX, T> *>(warp_smem);
@@ -736,7 +737,7 @@ __global__ void __launch_bounds__(32 * warps_per_block<PMAX>, WARP_MIN_BLOCKS) l
     const int wib = threadIdx.x >> 5;
     WarpShared<PMAX, T> *W = &WS[wib];
     const int n = NC > 0 ? NC : A.n, p = NC > 0 ? PMAX : A.p;
-    const int slot = blockIdx.x * warps_per_block<PMAX> + wib;
+    const int slot = blockIdx.x * warps_per_block<PMAX, T> + wib;
     WarpAccess<PMAX, T> acc{n, p, lane, W};
     const uint32_t inv_mask = bitonic_inv_mask(lane);
     Ctl<PMAX> &C = W->C;

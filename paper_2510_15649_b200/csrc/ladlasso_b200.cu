@@ -86,7 +86,7 @@ Variant make_thread_variant()
 template <int P, int NC, typename T = double>
 Variant make_warp_variant()
 {
-    constexpr int wpb = lad::warps_per_block<P>;
+    constexpr int wpb = lad::warps_per_block<P, T>;
     return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, sizeof(lad::WarpShared<P, T>) * wpb, 32 * wpb, wpb};
 }
 
