@@ -373,7 +373,7 @@ def run_aux(a, world, rank, local):
         hx, hy, hl = (torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v) for v in steps_inputs[a.warmup + k])
         hosts.append((hx.numpy(), hy.numpy(), hl.numpy()))
     run_host = (lambda h: lad.solve_lp_batched(*h)) if a.solver == "lp" else (lambda h: lad.solve_brute_batched(*h))
-    run_host(tuple(v[:256] for v in hosts[0]))
+    run_host(hosts[0])  # untimed full-size warm-up (allocator and pool growth)
     barrier()
     t0 = time.perf_counter()
     for h in hosts:
