@@ -316,7 +316,7 @@ extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const doubl
 {
     if (!(sweep_tolerance > 0)) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
     if (max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
-    if (!start) return fail(LAD_E_INVALID, "start must be non-null");
+    if (!start && B > 0) return fail(LAD_E_INVALID, "start must be non-null");
     lad_locus_params prm;
     lad_default_params(&prm);
     prm.lambda_floor = lambda_floor;
@@ -343,7 +343,7 @@ extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *
 {
     if (!(sweep_tolerance > 0)) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
     if (max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
-    if (!start) return fail(LAD_E_INVALID, "start must be non-null");
+    if (!start && B > 0) return fail(LAD_E_INVALID, "start must be non-null");
     lad_locus_params prm;
     lad_default_params(&prm);
     prm.lambda_floor = lambda_floor;
@@ -624,8 +624,8 @@ extern "C" int lad_lp_solve_f64(const double *X, const double *Y, const double *
     if (pivot_rule != LAD_PIVOT_DANTZIG_BLAND && pivot_rule != LAD_PIVOT_BLAND)
         return fail(LAD_E_INVALID, "unknown pivot rule %d", pivot_rule);
     if (!(lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
+    if (B == 0) return LAD_OK;  // (empty outputs may be null)
     if (!beta || !objective || !pivots || !converged || !status) return fail(LAD_E_INVALID, "output pointers must be non-null");
-    if (B == 0) return LAD_OK;
     const int warp_doubles = lad::lp_warp_doubles(n, p);
     const size_t smem = (size_t)lad::LP_WARPS * warp_doubles * sizeof(double);
     CK(cudaFuncSetAttribute(lad::lp_simplex_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -1,0 +1,97 @@
+"""Edge inputs through every batched entry point: empty batches, read-only and non-contiguous
+host arrays, device tensors, and agreement between the host-array and device-tensor paths.
+
+The reference's datasets are frozen read-only float64 arrays (model.py:32-39); host arrays go
+through lad_copy_h2d (a copy from the caller's own pointer) and come back in page-locked
+arrays, so both must be exercised for every call, as must B = 0 (a shard of an empty range in
+the multi-GPU split, distributed.shard_range).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2510_15649_b200 as lad  # noqa: E402
+
+
+def _problems(B, n=12, p=3, seed=3):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((B, n, p))
+    Y = X @ np.array([1.5, 0.0, -2.0][:p]) + rng.laplace(0, 0.4, (B, n))
+    L = rng.uniform(0.1, 1.5, B)
+    return X, Y, L
+
+
+CALLS = {
+    "locus": lambda X, Y, L, b: lad.solve_locus_batched(X, Y, L).objective,
+    "ccd": lambda X, Y, L, b: lad.ccd_descend_batched(X, Y, L, b).objective,
+    "brute": lambda X, Y, L, b: lad.solve_brute_batched(X, Y, L)[1],
+    "lp": lambda X, Y, L, b: lad.solve_lp_batched(X, Y, L).objective,
+    "objective": lambda X, Y, L, b: lad.evaluate_objective_batched(X, Y, L, b),
+    "certificate": lambda X, Y, L, b: lad.axiswise_minimum_batched(X, Y, L, b),
+}
+
+
+def _np(a):
+    return a.cpu().numpy() if torch.is_tensor(a) else np.asarray(a)
+
+
+@pytest.mark.parametrize("name", sorted(CALLS))
+def test_empty_batch_host_and_device(name):
+    X, Y, L = _problems(0)
+    b = np.zeros((0, 3))
+    out = CALLS[name](X, Y, L, b)
+    assert _np(out).shape[0] == 0
+    dev = [torch.from_numpy(a).cuda() for a in (X, Y, L, b)]
+    out = CALLS[name](*dev)
+    assert _np(out).shape[0] == 0
+
+
+@pytest.mark.parametrize("name", sorted(CALLS))
+def test_read_only_and_strided_host_arrays_match_device(name):
+    X, Y, L = _problems(64)
+    b = np.random.default_rng(5).standard_normal((64, 3))
+    ref = _np(CALLS[name](*[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (X, Y, L, b)]))
+    ro = [a.copy() for a in (X, Y, L, b)]
+    for a in ro:
+        a.setflags(write=False)
+    assert np.array_equal(_np(CALLS[name](*ro)), ref), "read-only host arrays"
+    # the same values through non-contiguous views (column-reversed storage, every other row of a wider array)
+    Xw = np.empty((64, 12, 6))
+    Xw[:, :, ::2] = X
+    Yw = np.empty((128, 12))
+    Yw[::2] = Y
+    Lw = np.empty(192)
+    Lw[::3] = L
+    bw = np.empty((64, 6))
+    bw[:, 1::2] = b
+    assert not (Xw[:, :, ::2].flags.c_contiguous or Lw[::3].flags.c_contiguous or bw[:, 1::2].flags.c_contiguous)
+    out = CALLS[name](Xw[:, :, ::2], Yw[::2], Lw[::3], bw[:, 1::2])
+    assert np.array_equal(_np(out), ref), "strided host arrays"
+
+
+def test_host_results_are_ordinary_writable_arrays():
+    X, Y, L = _problems(8)
+    r = lad.solve_locus_batched(X, Y, L)
+    beta, obj, nv = lad.solve_brute_batched(X, Y, L)
+    for a in (r.beta, r.objective, beta, obj, nv):
+        assert isinstance(a, np.ndarray) and a.flags.writeable and a.flags.c_contiguous
+    r.beta[0, 0] = 1.0  # results own their (page-locked) memory
+    beta[0, 0] = 1.0
+
+
+def test_float32_host_arrays_go_to_the_fp32_mode_and_float64_stays_exact(oracle):
+    """dtype selects the path: float64 in -> reference arithmetic, float32 in -> fp32 mode."""
+    X, Y, L = _problems(16)
+    r64 = lad.solve_locus_batched(X, Y, L)
+    o64 = oracle.solve_locus_batch(X, Y, L)
+    assert np.array_equal(r64.objective, o64["objective"])
+    Xf, Yf, Lf = (a.astype(np.float32) for a in (X, Y, L))
+    r32 = lad.solve_locus_batched(Xf, Yf, Lf)
+    o32 = oracle.solve_locus_batch(Xf, Yf, Lf)
+    assert r32.objective.dtype == np.float64 and np.array_equal(r32.objective, o32["objective"])
