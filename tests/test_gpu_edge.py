@@ -95,3 +95,38 @@ def test_float32_host_arrays_go_to_the_fp32_mode_and_float64_stays_exact(oracle)
     r32 = lad.solve_locus_batched(Xf, Yf, Lf)
     o32 = oracle.solve_locus_batch(Xf, Yf, Lf)
     assert r32.objective.dtype == np.float64 and np.array_equal(r32.objective, o32["objective"])
+
+
+def _degenerate_cases():
+    rng = np.random.default_rng(21)
+    n, p = 10, 3
+    base_X = rng.standard_normal((n, p))
+    base_y = base_X @ np.array([1.0, -2.0, 0.5]) + rng.laplace(0, 0.3, n)
+    cases = []
+    cases.append(("all-zero design", np.zeros((n, p)), base_y, 0.5))
+    cases.append(("lambda 0 (floor 1e-9)", base_X, base_y, 0.0))
+    cases.append(("lambda above max column sum", base_X, base_y, 2.0 * np.abs(base_X).sum(axis=0).max()))
+    cases.append(("duplicated rows", np.repeat(base_X[:5], 2, axis=0), np.repeat(base_y[:5], 2), 0.3))
+    cases.append(("y identically zero", base_X, np.zeros(n), 0.3))
+    cases.append(("one row", base_X[:1], base_y[:1], 0.3))
+    cases.append(("one column", base_X[:, :1], base_y, 0.3))
+    Xc = base_X.copy()
+    Xc[:, 1] = 1.0  # a constant column
+    cases.append(("constant column", Xc, base_y, 0.3))
+    return cases
+
+
+@pytest.mark.parametrize("case", range(8))
+@pytest.mark.parametrize("variant", ["ternary", "quadrature"])
+def test_degenerate_problems_bit_exact(oracle, case, variant):
+    name, x, y, lam = _degenerate_cases()[case]
+    X, Y, L = x[None].copy(), y[None].copy(), np.array([lam])
+    r = lad.solve_locus_batched(X, Y, L, lad.LocusConfig(outer_search=variant))
+    o = oracle.solve_locus_batch(X, Y, L, outer_search=variant)
+    assert np.array_equal(r.status, o["status"]), name
+    if o["status"][0] == 0:
+        assert np.array_equal(r.beta, o["beta"]) and np.array_equal(r.objective, o["objective"]), name
+        assert (r.steps[0], r.descents[0], r.iterations[0]) == (o["steps"][0], o["descents"][0], o["iterations"][0])
+    d = lad.ccd_descend_batched(X, Y, L, np.zeros((1, x.shape[1])))
+    od = oracle.ccd_descend(x, y, max(lam, 1e-9), np.zeros(x.shape[1]))
+    assert np.array_equal(d.beta[0], od.beta) and d.objective[0] == od.objective, name
