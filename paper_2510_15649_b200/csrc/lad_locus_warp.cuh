@@ -460,7 +460,8 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     // per sum) both sums are exact warp reductions, and a decision made with
     // a 2^14-unit (1.5e-5 * total) margin on both sides is the reference's
     // decision; it also excludes the 1e-12 * total midpoint tie.  Otherwise
-    // the full order + scan below decides.
+    // the walk below finds the median, and as a last resort (margin cases, an
+    // axis' first step, sparse columns) the full order + scan decides.
     T t_new;
     bool hit = false;
     if (cacheable) {
@@ -477,7 +478,7 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
             if (qb > hq + MEDIAN_MARGIN_Q) return -1;
             return 2;
         };
-        // first candidate (the hit path: ~85% of steps decide here)
+        // first candidate (the hit path: ~83% of config-2 steps decide here)
         t_new = shfl_t(loc, m1);
         const bool below1 = (loc < t_new) | ((loc == t_new) & (lane < m1));
         const unsigned qb1 = __reduce_add_sync(FULLMASK, below1 ? q : 0u);
