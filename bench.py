@@ -545,7 +545,7 @@ def main():
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"config{a.config}_{a.dtype}")
         if tr:
-            traffic = tr["bytes_per_solve"] * solves_per_step
+            traffic = tr["bytes_per_solve"] * wl.solves  # per launch (one call per variant and step)
             ipc = tr.get("warp_instr_per_coord_step")
             if ipc and clocks.get("sm_mhz"):
                 sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -603,7 +603,7 @@ def main():
                        "l2": "flushed between steps (256 MiB memset)"},
             "roofline": {"bound": "fp64" if a.dtype == "f64" else "fp32", "achieved": achieved_tflops, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None, "traffic": traffic,
-                         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per solve x solves per launch)",
+                         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per solve) x solves per launch",
                          "peak_source": (f"measured {'DFMA' if a.dtype == 'f64' else 'FFMA'} loop on this GPU "
                                          f"(lad_{a.dtype.replace('f', 'fp')}_peak_tflops); "
                                          "MEASURED_PEAKS.json has no FP64/FP32 CUDA-core figure"),
