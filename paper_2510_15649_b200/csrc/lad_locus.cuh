@@ -76,6 +76,7 @@ struct LocusArgs {
     int axis_mode;
     double *axis_res;   // (B * p) entries of axis_stride doubles
     int axis_stride;
+    unsigned *axis_done;  // (B,) finished axis searches per problem (AXIS_SEARCH); the last one runs the finish
 };
 
 template <int PMAX>
@@ -99,12 +100,15 @@ enum : int {
     PC_PR_AFTER_REFINE, PC_PR_FINISH,
     PC_DESC_AFTER,
     PC_FINISH_AXES,
+    PC_AXIS_COUNT,
 };
 
 // axis-parallel mode for small batches: the per-axis searches of solve_locus
 // share no state (locus.py:223-225), so they run as independent work items;
 // a finish pass replays them through the agreement rule in order.
-enum : int { AXIS_SERIAL = 0, AXIS_SEARCH = 1, AXIS_FINISH = 2 };
+// AXIS_SEARCH: one work item per (problem, axis); the unit that completes a
+// problem's last axis search finishes the problem (PC_AXIS_COUNT)
+enum : int { AXIS_SERIAL = 0, AXIS_SEARCH = 1 };
 
 enum : int { ACT_DESCENT = 0, ACT_EXIT = 1 };
 
@@ -113,6 +117,7 @@ struct Ctl {
     // problem
     int64_t prob;
     int arank;  // axis rank of an AXIS_SEARCH item
+    int replay; // AXIS_SEARCH: this warp is finishing its problem from the stored axis results
     double lam;
     uint32_t sparse_mask;
     int pc, ret_pc;
@@ -313,6 +318,14 @@ struct ThreadAccess {
     double *Xs, *Ys;
     __device__ __forceinline__ bool leader() const { return true; }
     __device__ __forceinline__ void sync() const {}
+    // count one finished unit on *ctr; true for the caller that completes `of` units
+    __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
+    {
+        __threadfence();
+        const bool last = atomicAdd(ctr, 1u) == of - 1u;
+        __threadfence();
+        return last;
+    }
     __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
         const int div = A.axis_mode == AXIS_SEARCH ? p : 1;
@@ -389,6 +402,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             if (got < 0) return ACT_EXIT;
             C.D = 0;
             C.S = 0;
+            C.replay = 0;
             if (got == 0) continue;  // invalid problem: status written, fetch the next one
             const int64_t pr = C.prob;
             if (A.mode == MODE_DESCENT) {
@@ -439,31 +453,55 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                 C.a_idx = C.arank;
                 C.pc = PC_AXIS_START;
             } else {
-                C.pc = A.axis_mode == AXIS_FINISH ? PC_FINISH_AXES : PC_AXIS_START;
+                C.pc = PC_AXIS_START;
             }
             break;
         }
         // axis-parallel finish: replay the stored per-axis results in influence
         // order through the same agreement rule (locus.py:338-362)
         case PC_FINISH_AXES: {
+            // written by other warps of this launch (fused finish): read through L2
             const double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
             C.axis = C.axes[C.a_idx];
-            C.ev_best.t = res[0];
-            for (int j = 0; j < p; ++j) C.ev_best.beta[j] = res[1 + j];
-            C.ev_best.value = res[1 + PMAX];
-            C.ev_best.conv = (int)res[2 + PMAX];
-            C.orounds = (int)res[3 + PMAX];
-            C.ev_calls = (int)res[4 + PMAX];
-            C.ev_failures = (int)res[5 + PMAX];
-            C.oconv = (int)res[6 + PMAX];
-            C.D += (int)res[7 + PMAX];
-            C.S += (long long)res[8 + PMAX];
+            C.ev_best.t = __ldcg(res + 0);
+            for (int j = 0; j < p; ++j) C.ev_best.beta[j] = __ldcg(res + 1 + j);
+            C.ev_best.value = __ldcg(res + 1 + PMAX);
+            C.ev_best.conv = (int)__ldcg(res + 2 + PMAX);
+            C.orounds = (int)__ldcg(res + 3 + PMAX);
+            C.ev_calls = (int)__ldcg(res + 4 + PMAX);
+            C.ev_failures = (int)__ldcg(res + 5 + PMAX);
+            C.oconv = (int)__ldcg(res + 6 + PMAX);
+            C.D += (int)__ldcg(res + 7 + PMAX);
+            C.S += (long long)__ldcg(res + 8 + PMAX);
             if (C.oconv < 0) {  // this axis' bracket expansion failed: raise here, as the serial scan does
                 write_unbounded<PMAX>(A, C, p, acc.leader());
                 C.pc = PC_FETCH;
                 break;
             }
             C.pc = PC_AXIS_DONE;
+            break;
+        }
+        // The unit that completes a problem's last axis search replays all of
+        // them through the agreement rule, refine and polish right away: the
+        // finish of one problem overlaps the other problems' searches, and the
+        // problem is still loaded.  Same states as a separate finish pass.
+        case PC_AXIS_COUNT: {
+            const bool last = acc.last_of(A.axis_done + C.prob, (unsigned)C.naxes);
+            acc.sync();
+            if (!last) {
+                C.pc = PC_FETCH;
+                break;
+            }
+            C.replay = 1;
+            C.a_idx = 0;
+            C.best_axis = C.axes[0];
+            C.nvals = C.rounds = C.calls = C.failures = 0;
+            C.outer_ok = 1;
+            C.confirmations = 0;
+            C.D = 0;  // the replay adds every axis' D and S
+            C.S = 0;
+            C.pc = PC_FINISH_AXES;
+            acc.sync();
             break;
         }
         case PC_DESC_AFTER: {
@@ -495,17 +533,18 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
         case PC_EX_2: C.g_hi = C.probe_v; C.ex_it = 0; C.pc = PC_EX_LOOP; break;
         case PC_EX_LOOP: {
             if (C.ex_it >= 60) {  // UnboundedDirectionError (linesearch.py:266)
-                if (A.axis_mode == AXIS_SEARCH) {
-                    // record it; the finish pass raises it when this axis' turn comes
+                if (A.axis_mode == AXIS_SEARCH && !C.replay) {
+                    // record it; the finish raises it when this axis' turn comes
                     if (acc.leader()) {
                         double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
                         res[6 + PMAX] = -1.0;
                         res[7 + PMAX] = C.D;
                         res[8 + PMAX] = (double)C.S;
                     }
-                } else {
-                    write_unbounded<PMAX>(A, C, p, acc.leader());
+                    C.pc = PC_AXIS_COUNT;
+                    break;
                 }
+                write_unbounded<PMAX>(A, C, p, acc.leader());
                 C.pc = PC_FETCH;
                 break;
             }
@@ -587,7 +626,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
         }
         // axis agreement bookkeeping (locus.py:338-362)
         case PC_AXIS_DONE: {
-            if (A.axis_mode == AXIS_SEARCH) {  // store this axis' result; the finish pass combines them
+            if (A.axis_mode == AXIS_SEARCH && !C.replay) {  // store this axis' result; the finish combines them
                 if (acc.leader()) {
                     double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
                     res[0] = C.ev_best.t;
@@ -601,7 +640,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                     res[7 + PMAX] = C.D;
                     res[8 + PMAX] = (double)C.S;
                 }
-                C.pc = PC_FETCH;
+                C.pc = PC_AXIS_COUNT;
                 break;
             }
             Point<PMAX> &ab = C.ev_best;
@@ -626,7 +665,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             if (p > 3 && C.confirmations >= 2) brk = true;
             C.a_idx++;
             C.pc = (brk || C.a_idx >= C.naxes) ? PC_REFINE_START
-                                                : (A.axis_mode == AXIS_FINISH ? PC_FINISH_AXES : PC_AXIS_START);
+                                                : (A.axis_mode != AXIS_SERIAL ? PC_FINISH_AXES : PC_AXIS_START);
             break;
         }
         // dense refinement plan (locus.py:363-395)

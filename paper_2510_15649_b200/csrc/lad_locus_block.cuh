@@ -175,6 +175,19 @@ struct BlockAccess {
     BlockMem<PMAX> M;
     __device__ __forceinline__ bool leader() const { return threadIdx.x == 0; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
+    {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            M.H->bci[3] = (int)(atomicAdd(ctr, 1u) == of - 1u);
+            __threadfence();
+        }
+        __syncthreads();
+        const bool last = M.H->bci[3] != 0;
+        __syncthreads();
+        return last;
+    }
     __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
         BlockHead<PMAX> *H = M.H;

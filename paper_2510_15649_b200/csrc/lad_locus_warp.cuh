@@ -183,6 +183,19 @@ struct WarpAccess {
     WarpShared<PMAX, T> *W;
     __device__ __forceinline__ bool leader() const { return lane == 0; }
     __device__ __forceinline__ void sync() const { __syncwarp(); }
+    // count one finished unit on *ctr (lane 0, after the warp's global writes are
+    // fenced); true in every lane for the warp that completes `of` units
+    __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
+    {
+        __syncwarp();
+        unsigned old = 0;
+        if (lane == 0) {
+            __threadfence();
+            old = atomicAdd(ctr, 1u);
+            __threadfence();
+        }
+        return __shfl_sync(FULLMASK, old, 0) == of - 1u;
+    }
     __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
         const int div = A.axis_mode == AXIS_SEARCH ? p : 1;

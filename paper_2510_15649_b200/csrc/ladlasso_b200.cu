@@ -245,29 +245,27 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     size_t seen_bytes = (size_t)slots * A.seen_cap * (1 + v.pmax) * sizeof(double);
     A.axis_stride = v.pmax + 10;
     size_t axis_bytes = axis_par ? (size_t)B * p * A.axis_stride * sizeof(double) : 0;
-    size_t scratch = 256 + seen_bytes + axis_bytes;
+    size_t done_bytes = axis_par ? (size_t)B * sizeof(unsigned) : 0;
+    size_t scratch = 256 + seen_bytes + axis_bytes + done_bytes;
     char *buf = nullptr;
     CK(cudaMallocAsync((void **)&buf, scratch, st));
     A.counter = (unsigned long long *)buf;
     A.seen = A.seen_cap ? (double *)(buf + 256) : nullptr;
     A.axis_res = axis_par ? (double *)(buf + 256 + seen_bytes) : nullptr;
+    A.axis_done = axis_par ? (unsigned *)(buf + 256 + seen_bytes + axis_bytes) : nullptr;
     CK(cudaMemsetAsync(buf, 0, 256, st));
+    if (axis_par) CK(cudaMemsetAsync(A.axis_done, 0, done_bytes, st));
     cudaError_t le;
     if (!axis_par) {
         A.axis_mode = lad::AXIS_SERIAL;
         v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A); ++g_launches;
         le = cudaGetLastError();
     } else {
+        // one launch: the per-axis searches as work items, each problem's finish
+        // (agreement, refine, polish) run by the warp that completes its last search
         A.axis_mode = lad::AXIS_SEARCH;
         v.fn<<<(unsigned)grid, v.block, v.smem, st>>>(A); ++g_launches;
         le = cudaGetLastError();
-        A.axis_mode = lad::AXIS_FINISH;
-        A.counter = (unsigned long long *)(buf + 64);
-        int64_t grid2 = std::min<int64_t>((B + v.slots_per_block - 1) / v.slots_per_block, max_grid);
-        if (le == cudaSuccess) {
-            v.fn<<<(unsigned)grid2, v.block, v.smem, st>>>(A); ++g_launches;
-            le = cudaGetLastError();
-        }
     }
     cudaFreeAsync(buf, st);
     if (le != cudaSuccess) return fail(LAD_E_CUDA, "locus kernel launch: %s", cudaGetErrorString(le));
