@@ -204,8 +204,12 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     const int64_t max_grid = (int64_t)g_num_sms * per_sm;
     // Small batches leave most warps idle and are bound by one solve's latency:
     // run the independent per-axis searches as separate work items (warp kernel).
+    // Up to two waves of problems it also wins: the finer items fill the grid's
+    // tail (scripts/axis_threshold.py: B = 8,192 +11% for config 2 shapes, +5%
+    // for config 4; equal at 16,384), despite searching every axis where the
+    // serial scan stops after two confirmations.
     const bool axis_par = g_axis_parallel && mode == lad::MODE_LOCUS && v.block > 32 && prm->outer_axis < 0 &&
-                          p > 1 && (g_axis_parallel == 2 || B < max_grid * v.slots_per_block);
+                          p > 1 && (g_axis_parallel == 2 || B < 2 * max_grid * v.slots_per_block);
     const int64_t items = axis_par ? B * p : B;
     int64_t want = (items + v.slots_per_block - 1) / v.slots_per_block;
     int64_t grid = std::min<int64_t>(want, max_grid);
