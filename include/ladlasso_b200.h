@@ -71,9 +71,10 @@ typedef struct lad_locus_out {
     int64_t *steps;           /* (B,) exact coordinate steps (may be NULL) */
 } lad_locus_out;
 
-#define LAD_KERNEL_AUTO 0   /* warp-per-problem for n <= 31, thread-per-problem for (n,p) = (10,2) */
+#define LAD_KERNEL_AUTO 0   /* warp-per-problem for n <= 31, thread-per-problem for (n,p) = (10,2),
+                               block-per-problem for 32 <= n <= 1023 */
 #define LAD_KERNEL_THREAD 1 /* one thread per problem (n <= 32) */
-#define LAD_KERNEL_WARP 2   /* one warp per problem, lane = row (n <= 31) */
+#define LAD_KERNEL_WARP 2   /* one warp per problem, lane = row (n <= 31; larger n: block per problem) */
 
 int lad_version(void);
 const char *lad_last_error(void);
