@@ -37,6 +37,8 @@ def _to_device(a, dev):
     import torch
 
     a = np.ascontiguousarray(a)
+    if not a.dtype.isnative:  # the copy moves raw bytes: bring foreign byte order to native first
+        a = a.astype(a.dtype.newbyteorder("="))
     t = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), device=dev)
     _check(_lib.load().lad_copy_h2d(t.data_ptr(), a.ctypes.data, a.nbytes, torch.cuda.current_stream(dev).cuda_stream))
     return t

@@ -130,3 +130,11 @@ def test_degenerate_problems_bit_exact(oracle, case, variant):
     d = lad.ccd_descend_batched(X, Y, L, np.zeros((1, x.shape[1])))
     od = oracle.ccd_descend(x, y, max(lam, 1e-9), np.zeros(x.shape[1]))
     assert np.array_equal(d.beta[0], od.beta) and d.objective[0] == od.objective, name
+
+
+def test_big_endian_host_arrays():
+    X, Y, L = _problems(16)
+    ref = lad.solve_brute_batched(X, Y, L)[1]
+    be = [a.astype(a.dtype.newbyteorder(">")) for a in (X, Y, L)]
+    assert np.array_equal(lad.solve_brute_batched(*be)[1], ref)
+    assert np.array_equal(lad.solve_locus_batched(*be).objective, lad.solve_locus_batched(X, Y, L).objective)
