@@ -545,7 +545,8 @@ def main():
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"config{a.config}_{a.dtype}")
         if tr:
-            traffic = tr["bytes_per_solve"] * wl.solves  # per launch (one call per variant and step)
+            if tr.get("bytes_per_solve") is not None:
+                traffic = tr["bytes_per_solve"] * wl.solves  # per launch (one call per variant and step)
             ipc = tr.get("warp_instr_per_coord_step")
             if ipc and clocks.get("sm_mhz"):
                 sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -556,7 +557,7 @@ def main():
                          "warp_instr_per_coord_step": ipc,
                          "source": "instr/step from profiles/ncu_traffic.json x live coordinate steps/s; "
                                    "peak = 4 SMSPs x SMs x sampled SM clock"}
-    except (OSError, ValueError):
+    except (OSError, ValueError, KeyError, TypeError):
         pass
     cpu = None
     parity = None
