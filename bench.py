@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
     ap.add_argument("--solver", choices=["locus", "lp", "brute"], default="locus",
                     help="locus (the metric); lp = the simplex on config-2 problems; brute = the check on config 1")
+    ap.add_argument("--warm", action="store_true",
+                    help="config 2 warm-start lambda path (previous lambda's solution seeds the bracket)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend for the barrier / max-reduce (gloo: the 1-GPU multi-rank test)")
     ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
                     help="f32: the fp32 mode (binary32 data and descents; config 4 runs in both)")
     return ap.parse_args()
@@ -156,51 +160,124 @@ def variants_of(a, config):
     return ["ternary", "quadrature"] if v == "both" else [v]
 
 
-def run_cpu_sample(X, Y, datasets, variants):
-    """Oracle (CPU restatement of the reference) on datasets x 16 lambdas x variants, all host threads."""
+CPU_SAMPLE = {0: 256, 1: 1 << 16, 2: 128, 3: 2048, 4: 256}  # per step: solves (config 2: datasets x 16 lambdas)
+SEEDS = {c: 15649 + c for c in range(5)}
+
+
+def block_for_step(step, world, rank, nblocks):
+    """Weak-scaling schedule (paper_2510_15649_b200.distributed.block_for_step, restated here so the
+    reference arm imports nothing from the product package)."""
+    return (step * world + rank) % nblocks
+
+
+def shard_range(B, world, rank):
+    """Contiguous shard of rank (paper_2510_15649_b200.distributed.shard_range)."""
+    base, extra = divmod(B, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def step_first(config, a, s, world, rank):
+    """First problem (config 2: first dataset) of bench step s on `rank` -- shared by both arms."""
+    if config == 2:
+        return block_for_step(s, world, rank, TOTAL_DATASETS // a.block) * a.block
+    if config == 3:
+        return shard_range(142506, world, rank)[0]
+    return (s * world + rank) * {0: 256, 1: 1 << 20, 4: a.block4}[config]
+
+
+def workload_config(config, a, world):
+    """The workload description both arms print (identical dicts: the driver compares them)."""
+    variants = variants_of(a, config)
+    n, p = {0: (30, 5), 1: (10, 2), 2: (30, 5), 3: (25, 5), 4: (31, 8)}[config]
+    if config == 2:
+        desc = (f"config 2 lambda path: 2^20 datasets (n=30, p=5, config-0 distributions) x 16 lambdas 1e-2..1e1; "
+                f"step = {a.block} datasets x 16 lambdas x {'+'.join(variants)}")
+        solves = a.block * 16
+    elif config == 3:
+        s0, e0 = shard_range(142506, world, 0)
+        desc = "config 3: C(30,25)=142506 row subsets of one dataset, lambda=0.5, quadrature"
+        solves = e0 - s0
+    else:
+        solves = {0: 256, 1: 1 << 20, 4: a.block4}[config]
+        desc = {0: "config 0: B=256, n=30, p=5, lambda=1, ternary",
+                1: "config 1: B=2^20, n=10, p=2, lambda~U(0.1,2), thread-per-problem kernel",
+                4: f"config 4: n=31, p=8, Student-t(3) X, Cauchy noise, lambda=1; step = {solves} of the 2^26 problems"}[config]
+    cfg = {"workload": f"config{config}", "description": desc, "n": n, "p": p,
+           "solves_per_step_per_gpu": solves * len(variants), "variant": "+".join(variants),
+           "dtype": a.dtype, "parallelism": f"shard{world} (independent problems, no collective)",
+           "inputs": f"seeded synthetic (Philox keyed by seed {SEEDS[config]} and problem index)"}
+    if a.warm:
+        cfg["warm"] = True
+    return cfg
+
+
+def host_step_problems(config, a, s, world, rank, limit):
+    """The first `limit` solves' inputs of bench step s, generated on the HOST by the oracle's
+    restatement of the device generator (oracle/gen_host.c; byte-identical to lad_generate_f64,
+    tests/test_gpu_generator.py) -- the reference arm never loads the product library."""
     from oracle import oracle as O
 
-    O.build()
-    Xs = np.repeat(X[:datasets], 16, axis=0)
-    Ys = np.repeat(Y[:datasets], 16, axis=0)
-    L = np.tile(LAMBDA_GRID, datasets)
-    nth = cpu_threads()
-    t0 = time.perf_counter()
-    r = [O.solve_locus_batch(Xs, Ys, L, nthreads=nth, outer_search=v) for v in variants]
-    dt = time.perf_counter() - t0
-    return r, dt, nth, Xs.shape[0] * len(variants)
+    first = step_first(config, a, s, world, rank)
+    if config == 2:
+        X, Y, _ = O.generate(2, limit, SEEDS[2], first)
+        return np.repeat(X, 16, axis=0), np.repeat(Y, 16, axis=0), np.tile(LAMBDA_GRID, limit)
+    if config == 3:
+        X0, Y0 = O.config3_dataset(SEEDS[3])
+        X, Y = O.subsets(X0, Y0, 25, first, limit)
+        return X, Y, np.full(limit, 0.5)
+    return O.generate(config, limit, SEEDS[config], first)
 
 
 def run_reference(a, rank, world):
-    """Reference arm: the CPU path (oracle port of solve_locus) on the host cores; rank 0 only."""
+    """Reference arm: the reference's solve_locus restated on the CPU (the oracle, a C port pinned
+    bit-exact to the reference) on all host threads, on a bounded sample of each bench step's
+    problems generated on the host; rank 0 only.  Loads no product code (no torch either)."""
     if rank != 0:
         return
-    import torch  # noqa: F401  (device generator provides the identical problem bytes)
-    from paper_2510_15649_b200 import configgen as G
+    from oracle import oracle as O
 
-    variants = variants_of(a, 2)
-    per_step = max(1, min(a.cpu_sample, 256 // len(variants)))  # 4,096 solves (~1.3 s on 16 threads) per step
+    O.build()
+    config = a.config
+    variants = variants_of(a, config)
+    limit = CPU_SAMPLE[config] // (1 if config == 2 else len(variants))
+    nth = cpu_threads()
+    fp32 = a.dtype == "f32"
     times, solves = [], 0
     for s in range(a.warmup + a.steps):
-        Xd, Yd, _ = G.generate(2, per_step, seed=SEED, first=(s * a.block) % TOTAL_DATASETS)
-        X, Y = Xd.cpu().numpy(), Yd.cpu().numpy()
-        _, dt, nth, ns = run_cpu_sample(X, Y, per_step, variants)
+        X, Y, L = host_step_problems(config, a, s, world, rank, limit)
+        if fp32:
+            X, Y, L = X.astype(np.float32), Y.astype(np.float32), L.astype(np.float32)
+        t0 = time.perf_counter()
+        for v in variants:
+            O.solve_locus_batch(X, Y, L, nthreads=nth, outer_search=v)
+        dt = time.perf_counter() - t0
         if s >= a.warmup:
             times.append(dt)
-            solves += ns
+            solves += X.shape[0] * len(variants)
     total = sum(times)
     value = solves / total
-    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "solves/s", "n_gpus": world,
+    per = solves // a.steps
+    sample = (f"first {per // len(variants)} solves of each bench step "
+              f"({limit} datasets x 16 lambdas)" if config == 2 else f"first {per // len(variants)} problems of each bench step")
+    line = {"metric": metric_name(a), "impl": "reference", "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device Philox generator, BASELINE config 2 distributions)",
-            "config": {"workload": "config2", "n": N_ROWS, "p": N_FEAT, "lambdas": 16,
-                       "variant": "+".join(variants), "solves_per_step": per_step * 16 * len(variants)},
+            "scaling": "weak" if config != 3 else "strong", "vs_baseline": None, "dtype": a.dtype,
+            "data": "synthetic (host restatement of the device Philox generator, BASELINE config distributions)",
+            "config": workload_config(config, a, world),
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": nth, "kind": "port",
-                             "sample": f"{per_step} config-2 datasets x 16 lambdas x {'+'.join(variants)} per step, "
-                                       f"{a.steps} timed steps, CPU oracle (C restatement of solve_locus)"},
+                             "sample": f"{sample} x {'+'.join(variants)}, {a.steps} timed steps after {a.warmup} "
+                                       f"warm-up; CPU oracle (C restatement of solve_locus, pinned bit-exact to "
+                                       f"the reference){', binary32 build' if fp32 else ''} on {nth} threads"},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def metric_name(a):
+    if a.config == 2 and a.dtype == "f64" and not a.warm:
+        return METRIC
+    n, p = {0: (30, 5), 1: (10, 2), 2: (30, 5), 3: (25, 5), 4: (31, 8)}[a.config]
+    return f"LAD-LASSO solves/sec (config {a.config}{' warm' if a.warm else ''}, n={n},p={p} {a.dtype.replace('f', 'fp')})"
 
 
 class Workload:
@@ -216,7 +293,6 @@ class Workload:
     def _build(self, config, a, world, rank, dev):
         import torch
         from paper_2510_15649_b200 import configgen as G
-        from paper_2510_15649_b200.distributed import block_for_step
 
         self.config = config
         self.variants = variants_of(a, config)
@@ -225,39 +301,28 @@ class Workload:
         self.data_index = None
         self.steps_inputs = []
         nsteps = a.warmup + a.steps
-        seed = SEED - 2 + config
+        solves = workload_config(config, a, world)["solves_per_step_per_gpu"] // len(self.variants)
         if config == 2:
             blk = a.block
-            self.desc = (f"config 2 lambda path: 2^20 datasets (n=30, p=5, config-0 distributions) x 16 lambdas "
-                         f"1e-2..1e1; step = {blk} datasets x 16 lambdas x {'+'.join(self.variants)}")
             for s in range(nsteps):
-                first = block_for_step(s, world, rank, TOTAL_DATASETS // blk) * blk
-                X, Y, _ = G.generate(2, blk, seed=SEED, first=first, device=dev)
+                X, Y, _ = G.generate(2, blk, seed=SEEDS[2], first=step_first(2, a, s, world, rank), device=dev)
                 self.steps_inputs.append((X, Y))
             self.data_index = torch.arange(blk, device=dev, dtype=torch.int64).repeat_interleave(16)
             self.lam = torch.tensor(LAMBDA_GRID, device=dev, dtype=torch.float64).repeat(blk)
-            self.solves = blk * 16
         elif config == 3:
-            X0, Y0 = G.config3_dataset(device=dev)
-            total = G.CONFIG_BATCH[3]
-            s0, e0 = [(total * r) // world for r in (rank, rank + 1)]
+            X0, Y0 = G.config3_dataset(seed=SEEDS[3], device=dev)
+            s0, e0 = shard_range(G.CONFIG_BATCH[3], world, rank)
             Xs, Ys = G.subsets(X0, Y0, 25, s0, e0 - s0)
-            self.desc = f"config 3: C(30,25)={total} row subsets of one dataset, lambda=0.5, quadrature"
             self.steps_inputs = [(Xs, Ys)] * nsteps
             self.lam = torch.full((e0 - s0,), 0.5, device=dev, dtype=torch.float64)
-            self.solves = e0 - s0
+            solves = e0 - s0
         else:
-            B = {0: 256, 1: 1 << 20, 4: a.block4}[config]
-            self.desc = {0: "config 0: B=256, n=30, p=5, lambda=1, ternary",
-                         1: "config 1: B=2^20, n=10, p=2, lambda~U(0.1,2), thread-per-problem kernel",
-                         4: f"config 4: n=31, p=8, Student-t(3) X, Cauchy noise, lambda=1; step = {B} of the 2^26 problems"}[config]
-            lam_step = None
             for s in range(nsteps):
-                first = (s * world + rank) * B
-                X, Y, L = G.generate(config, B, seed=seed, first=first, device=dev)
+                X, Y, L = G.generate(config, solves, seed=SEEDS[config], first=step_first(config, a, s, world, rank),
+                                     device=dev)
                 self.steps_inputs.append((X, Y, L))
             self.lam = None
-            self.solves = B
+        self.solves = solves
 
     def inputs(self, s):
         t = self.steps_inputs[s]
@@ -437,6 +502,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.warm and a.config != 2:
+        raise SystemExit("--warm is the config-2 lambda path mode")
     if a.impl == "reference":
         return run_reference(a, rank, world)
     if a.solver != "locus":
@@ -445,10 +512,11 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())  # ranks > GPUs only in the gloo test
+    torch.cuda.set_device(dev)
+    backend = a.dist_backend
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     import paper_2510_15649_b200 as lad
     from paper_2510_15649_b200 import _lib
     from paper_2510_15649_b200.solver import fp32_peak_tflops, fp64_peak_tflops
@@ -490,7 +558,7 @@ def main():
     clocks = clk.summary()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
     elapsed = sum(step_ms) / 1e3
-    t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+    t = torch.tensor([elapsed], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_max = float(t.item())
@@ -503,18 +571,19 @@ def main():
     status_ok = all(bool((r.status == 0).all()) for r in results)
     conv_frac = float(np.mean([float(r.converged.float().mean()) for r in results]))
 
-    # ---- end to end through the host-buffer C ABI (pinned host memory, copies inside)
-    e2e_steps = a.e2e_steps if a.e2e_steps is not None else min(a.steps, 3)
+    # ---- end to end through the host-buffer C ABI (pinned host memory, copies inside), over the
+    # same number of steps as the device-timed region
+    e2e_steps = a.e2e_steps if a.e2e_steps is not None else a.steps
     host = []
-    for k in range(e2e_steps):
-        X, Y, L = wl.inputs(a.warmup + k)
-        hx = torch.empty(X.shape, dtype=hdt, pin_memory=True)
-        hy = torch.empty(Y.shape, dtype=hdt, pin_memory=True)
-        hl = torch.empty(L.shape, dtype=hdt, pin_memory=True)
-        hx.copy_(X)
-        hy.copy_(Y)
-        hl.copy_(L)
-        host.append((hx.numpy(), hy.numpy(), hl.numpy()))
+    step_bytes = sum(t.numel() * (4 if a.dtype == "f32" else 8) for t in wl.inputs(a.warmup))
+    n_host = max(1, min(e2e_steps, (2 << 30) // max(1, step_bytes)))  # distinct steps within 2 GiB of pinned memory
+    for k in range(n_host):
+        bufs = []
+        for v in wl.inputs(a.warmup + k):
+            h = torch.empty(v.shape, dtype=hdt, pin_memory=True)
+            h.copy_(v)
+            bufs.append(h.numpy())
+        host.append(tuple(bufs))
     hidx_np = None
     if wl.data_index is not None:
         hidx = torch.empty(wl.data_index.shape, dtype=torch.int64, pin_memory=True)
@@ -526,16 +595,16 @@ def main():
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
+        h = host[k % n_host]
         for c in cfgs:  # each variant is one public-API call with its own H2D and D2H
-            lad.solve_locus_batched(host[k][0], host[k][1], host[k][2], c, data_index=hidx_np)
+            lad.solve_locus_batched(h[0], h[1], h[2], c, data_index=hidx_np)
     barrier()
     e2e_elapsed = time.perf_counter() - t0
-    te = torch.tensor([e2e_elapsed], device=dev, dtype=torch.float64)
+    te = torch.tensor([e2e_elapsed], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * e2e_steps * solves_per_step / float(te.item())
-    h2d = len(cfgs) * (host[0][0].nbytes + host[0][1].nbytes + host[0][2].nbytes +
-                       (hidx_np.nbytes if hidx_np is not None else 0))
+    h2d = len(cfgs) * (sum(x.nbytes for x in host[0]) + (hidx_np.nbytes if hidx_np is not None else 0))
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
 
     # DRAM traffic per launch and warp instructions per coordinate step from the committed
@@ -561,6 +630,7 @@ def main():
         pass
     cpu = None
     parity = None
+    fp32_dist = None
     if rank == 0 and world == 1 and not a.no_cpu:
         # ~10 s of CPU work per config on a 16-thread host (config 0 is the whole config)
         max_solves = {0: 256, 1: 1 << 20, 2: a.cpu_sample * 16, 3: 32768, 4: 8192}[a.config] // len(cfgs)
@@ -569,7 +639,8 @@ def main():
 
         O.build()
         nth = cpu_threads()
-        if a.dtype == "f32":
+        if a.dtype == "f32":  # the f32 workload's inputs are the fp64 problems rounded once
+            X64, Y64, L64 = Xh.astype(np.float64), Yh.astype(np.float64), np.asarray(Lh, dtype=np.float64)
             Xh, Yh, Lh = Xh.astype(np.float32), Yh.astype(np.float32), np.asarray(Lh, dtype=np.float32)
         t0 = time.perf_counter()
         ros = [O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=v) for v in wl.variants]
@@ -587,21 +658,32 @@ def main():
             exact += int(np.sum(np.all(gb == ro["beta"], axis=1) & (go == ro["objective"]) & (gs == ro["steps"])))
             rel = np.abs(go - ro["objective"]) / np.abs(ro["objective"])
             within += int(np.sum(rel <= 1e-9))
-        parity = {"sample": nsol * len(ros), "bit_exact": exact, "obj_within_1e-9": within}
+        parity = {"sample": nsol * len(ros), "bit_exact": exact, "obj_within_1e-9": within,
+                  "checker": "CPU oracle" + (" (binary32 build)" if a.dtype == "f32" else "")}
+        if a.dtype == "f32":
+            # the fp32 mode against the fp64 reference path (the oracle in binary64 = the reference
+            # bit for bit) on the unrounded problems: a reported statistic, not a parity claim
+            m = min(nsol, 1024)
+            r64 = O.solve_locus_batch(X64[:m], Y64[:m], L64[:m], nthreads=nth, outer_search=wl.variants[0])
+            g = results[0]
+            go = g.objective[:m].cpu().numpy()
+            rel = (go - r64["objective"]) / np.abs(r64["objective"])
+            sup = np.all((np.abs(g.beta[:m].cpu().numpy()) > 1e-6) == (np.abs(r64["beta"]) > 1e-6), axis=1)
+            fp32_dist = {"sample": m, "rel_obj_diff_max": float(np.max(np.abs(rel))),
+                         "rel_obj_diff_median": float(np.median(rel)), "rel_obj_diff_p99": float(np.quantile(np.abs(rel), 0.99)),
+                         "fp32_lower_frac": float(np.mean(rel < 0)), "support_equal_frac": float(np.mean(sup))}
 
     if rank == 0:
         line = {
-            "metric": METRIC if (a.config == 2 and a.dtype == "f64") else
-            f"LAD-LASSO solves/sec (config {a.config}, n={wl.n},p={wl.p} {a.dtype.replace('f', 'fp')})",
+            "metric": metric_name(a),
             "value": value, "unit": "solves/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": elapsed_max * 1e3 / a.steps, "higher_is_better": True,
             "scaling": "weak" if a.config != 3 else "strong", "vs_baseline": None, "dtype": a.dtype,
             "data": "synthetic (device Philox generator with the BASELINE config distributions)",
-            "config": {"workload": f"config{a.config}", "description": wl.desc, "n": wl.n, "p": wl.p,
-                       "solves_per_step_per_gpu": solves_per_step, "variant": "+".join(wl.variants),
-                       "parallelism": f"shard{world} (independent problems, no collective)",
-                       "kernel": "thread-per-problem sm_100a" if a.config == 1 else "warp-per-problem sm_100a",
-                       "l2": "flushed between steps (256 MiB memset)"},
+            "config": workload_config(a.config, a, world),
+            "kernel": {1: "locus_kernel<10,2,1> thread-per-problem sm_100a"}.get(
+                a.config, "locus_warp_kernel warp-per-problem sm_100a"),
+            "l2": "flushed between steps (256 MiB memset, outside the events)",
             "roofline": {"bound": "fp64" if a.dtype == "f64" else "fp32", "achieved": achieved_tflops, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None, "traffic": traffic,
                          "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per solve) x solves per launch",
@@ -614,7 +696,8 @@ def main():
             "issue_roofline": issue,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps, "distinct_input_steps": n_host},
+            "fp32_vs_fp64_reference": fp32_dist,
             "gpu_launches": gpu_launches,
             "clocks": clocks,
             "status_ok": status_ok,

@@ -382,6 +382,75 @@ def gen_configs(pool, quick=False):
     _locus_fixture(pool, "cfg4", X, Y, 1.0, ("ternary",), extra=dict(beta_true=bt))
 
 
+def gen_bench(pool, quick=False):
+    """The bench's ACTUAL inputs (bench.py seeds and block offsets, produced by the host
+    restatement of the device generator, oracle/gen_host.c, which tests/test_gpu_generator.py
+    pins byte-for-byte to lad_generate_f64) solved by the unmodified reference."""
+    import oracle as O  # oracle/oracle.py (this directory is on sys.path)
+
+    O.build()
+    k = 4 if quick else 1
+    # config 0: bench step 0 is problems [0, 256) of seed 15649, ternary
+    X, Y, lam, bt = O.generate(0, 256 // k, 15649, 0, with_beta=True)
+    _locus_fixture(pool, "bench_cfg0", X, Y, lam, ("ternary", "quadrature"), brute_idx=range(2),
+                   extra=dict(beta_true=bt, seed=15649, first=0))
+    # config 1: problems of the first and of a late bench step (seed 15650), both variants + brute
+    X1, Y1, L1 = O.generate(1, 192 // k, 15650, 0)
+    X2, Y2, L2 = O.generate(1, 64 // k, 15650, 7 << 20)
+    X, Y, lam = np.concatenate([X1, X2]), np.concatenate([Y1, Y2]), np.concatenate([L1, L2])
+    index = np.concatenate([np.arange(len(L1)), (7 << 20) + np.arange(len(L2))])
+    _locus_fixture(pool, "bench_cfg1", X, Y, lam, ("ternary", "quadrature"), brute_idx=range(len(lam)),
+                   extra=dict(seed=15650, problem_index=index))
+    # config 2: datasets of the first and the last bench block (16384 datasets each), all 16 lambdas
+    firsts = [0, 63 * 16384] if quick else [*range(8), *range(63 * 16384, 63 * 16384 + 4), 64 * 16384 - 4, 64 * 16384 - 3, 64 * 16384 - 2, 64 * 16384 - 1]
+    Xd = np.concatenate([O.generate(2, 1, 15651, f)[0] for f in firsts])
+    Yd = np.concatenate([O.generate(2, 1, 15651, f)[1] for f in firsts])
+    Xr, Yr = np.repeat(Xd, 16, axis=0), np.repeat(Yd, 16, axis=0)
+    lam = np.tile(configs_np.LAMBDA_GRID, len(firsts))
+    _locus_fixture(pool, "bench_cfg2", Xr, Yr, lam, ("ternary", "quadrature"),
+                   extra=dict(seed=15651, dataset_index=np.asarray(firsts)))
+    # config 3: the bench's dataset (seed 15652, problem 0) and subsets spread over all 142,506
+    X0, Y0 = O.config3_dataset(15652)
+    total = math.comb(30, 25)
+    ks = np.unique(np.concatenate([np.arange(4), np.linspace(0, total - 1, 44 // k).astype(np.int64)]))
+    Xs = np.concatenate([O.subsets(X0, Y0, 25, int(q), 1)[0] for q in ks])
+    Ys = np.concatenate([O.subsets(X0, Y0, 25, int(q), 1)[1] for q in ks])
+    _locus_fixture(pool, "bench_cfg3", Xs, Ys, 0.5, ("quadrature",), brute_idx=(0,),
+                   extra=dict(dataset_x=X0, dataset_y=Y0, subset_index=ks, seed=15652))
+    # config 4: bench step 0 problems (seed 15653), ternary
+    X, Y, lam, bt = O.generate(4, 64 // k, 15653, 0, with_beta=True)
+    _locus_fixture(pool, "bench_cfg4", X, Y, lam, ("ternary",), extra=dict(beta_true=bt, seed=15653, first=0))
+
+
+def _objective_task(args):
+    _ref()
+    from ladlasso.model import Coefficients, Dataset, ProblemSpec, evaluate_objective
+
+    x, y, lam, b = args
+    return evaluate_objective(ProblemSpec(Dataset(x, y), lam), Coefficients(b))
+
+
+def gen_objective(pool):
+    """model.evaluate_objective (model.py:151-154) on random coefficients, every p <= 8 and
+    row counts on both sides of numpy's 128-term pairwise block (up to 1000 rows)."""
+    rng = np.random.default_rng(151)
+    out = {}
+    for m, d in ((1, 1), (7, 2), (30, 5), (31, 8), (128, 3), (129, 4), (200, 6), (257, 7), (1000, 8), (1023, 1)):
+        B = 16 if m <= 257 else 4
+        X = rng.standard_normal((B, m, d)) * rng.choice([1e-3, 1.0, 1e3], size=(B, 1, 1))
+        Y = rng.standard_normal((B, m)) * 10
+        beta = rng.standard_normal((B, d))
+        beta[rng.random((B, d)) < 0.3] = 0.0
+        lam = rng.uniform(0.0, 3.0, B)
+        lam[0] = 0.0  # the 1e-9 floor
+        vals = pool.map(_objective_task, [(X[b], Y[b], float(lam[b]), beta[b]) for b in range(B)])
+        out[f"x_{m}_{d}"], out[f"y_{m}_{d}"], out[f"beta_{m}_{d}"] = X, Y, beta
+        out[f"lam_{m}_{d}"], out[f"objective_{m}_{d}"] = lam, np.array(vals)
+    out["shapes"] = np.array([[int(k.split("_")[1]), int(k.split("_")[2])] for k in out if k.startswith("x_")])
+    np.savez_compressed(os.path.join(GOLDEN, "objective.npz"), **out)
+    print("objective.npz", flush=True)
+
+
 def _run_ref_cli(argv):
     """Run the reference CLI in-process; return (exit code, stdout, stderr)."""
     import contextlib
@@ -637,7 +706,8 @@ def main():
     with Pool(a.procs) as pool:
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
-                         ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp), ("large", gen_large)):
+                         ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp), ("large", gen_large),
+                         ("bench", lambda p: gen_bench(p, a.quick)), ("objective", gen_objective)):
             if only is None or name in only:
                 fn(pool)
 

@@ -46,7 +46,7 @@ class LocusParams(C.Structure):
 
 
 def build(force: bool = False) -> str:
-    newest = max(os.path.getmtime(os.path.join(_HERE, f)) for f in ("ladlasso_oracle.c", "orc_descent.inc"))
+    newest = max(os.path.getmtime(os.path.join(_HERE, f)) for f in ("ladlasso_oracle.c", "orc_descent.inc", "gen_host.c", "Makefile"))
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
         subprocess.run(["make", "-s", "-C", _HERE, "liboracle.so"], check=True)
     return _LIB_PATH
@@ -102,6 +102,10 @@ def lib():
         L.orc_candidate_count.argtypes = [C.c_int, C.c_int]
         L.orc_solve_brute.restype = C.c_int
         L.orc_solve_brute.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_longlong, dp, dp, lp]
+        L.orc_generate.restype = C.c_int
+        L.orc_generate.argtypes = [C.c_int, C.c_uint64, C.c_longlong, C.c_longlong, C.c_int, C.c_int, dp, dp, dp, dp]
+        L.orc_subsets.restype = C.c_int
+        L.orc_subsets.argtypes = [dp, dp, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_longlong, dp, dp]
         _lib = L
     return _lib
 
@@ -349,3 +353,42 @@ def solve_brute(x, y, lam_eff, max_variables=6, max_candidates=2_000_000):
     if rc:
         raise ValueError(f"brute failed rc={rc}")
     return beta, obj.value, ev.value
+
+
+# ---- host restatement of the device config generator (oracle/gen_host.c) ----
+
+CONFIG_SHAPES = {0: (30, 5), 1: (10, 2), 2: (30, 5), 3: (25, 5), 4: (31, 8)}
+
+
+def generate(config: int, B: int, seed: int, first: int = 0, with_beta: bool = False):
+    """Problems [first, first + B) of BASELINE config 0/1/2/4, byte-identical to lad_generate_f64."""
+    n, p = CONFIG_SHAPES[config]
+    X = np.empty((B, n, p))
+    Y = np.empty((B, n))
+    lam = np.empty(B)
+    bt = np.empty((B, p))
+    dp = C.POINTER(C.c_double)
+    rc = lib().orc_generate(config, seed, first, B, n, p, X.ctypes.data_as(dp), Y.ctypes.data_as(dp),
+                            lam.ctypes.data_as(dp), bt.ctypes.data_as(dp))
+    if rc != 0:
+        raise ValueError(f"orc_generate: bad arguments (config {config})")
+    return (X, Y, lam, bt) if with_beta else (X, Y, lam)
+
+
+def subsets(X0, Y0, keep: int, first: int, B: int):
+    """Config 3: rows of the k-th keep-subsets (lexicographic), k in [first, first + B)."""
+    X0, px = _d(X0)
+    Y0, py = _d(Y0)
+    n0, p = X0.shape
+    X = np.empty((B, keep, p))
+    Y = np.empty((B, keep))
+    dp = C.POINTER(C.c_double)
+    if lib().orc_subsets(px, py, n0, p, keep, first, B, X.ctypes.data_as(dp), Y.ctypes.data_as(dp)) != 0:
+        raise ValueError("orc_subsets: bad arguments")
+    return X, Y
+
+
+def config3_dataset(seed: int = 15649 + 3):
+    """The one n=30, p=5 dataset of config 3 (config-0 problem 0 under config 3's seed)."""
+    X, Y, _ = generate(0, 1, seed)
+    return X[0], Y[0]

@@ -16,8 +16,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libladlasso_b200.so")
 SOURCES = ["ladlasso_b200.cu"]
-HEADERS = ["lad_numerics.cuh", "lad_sortnet.cuh", "lad_locus.cuh", "lad_locus_warp.cuh", "lad_brute.cuh",
-           "lad_gen.cuh"]
+
+
+def headers() -> list[str]:
+    """Every header under csrc/ counts toward staleness (the .cu includes them all)."""
+    return sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 NVCC_FLAGS = [
     "-std=c++17",
@@ -42,7 +45,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "ladlasso_b200.h")]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + headers()] + [os.path.join(ROOT, "include", "ladlasso_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

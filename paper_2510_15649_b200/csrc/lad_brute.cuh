@@ -181,7 +181,7 @@ __device__ __forceinline__ bool eval_vertex(const int (&c)[P], int m, double lam
         b[r] = pl < m ? yat(pl) : 0.0;
     }
     if (!solve_ge<P>(a, b, sol)) return false;
-    double rs = np_sum(m, [&](int i) {
+    double rs = np_sum(m, [&](int i) {  // m <= 64 here (lad_brute_solve_f64)
         double g = gemv_row(P, i, m, [&](int q) { return xat(i, q); }, [&](int q) { return sol[q < P ? q : P - 1]; });
         return fabs(dsub(yat(i), g));
     });
@@ -336,7 +336,7 @@ __global__ void objective_kernel(const double *X, const double *Y, const double 
     for (int q = 0; q < P; ++q) b[q] = beta[(size_t)pr * P + q];
     double lr = lamv[pr];
     double lam = lr > lambda_floor ? lr : lambda_floor;
-    double rs = np_sum(m, [&](int i) {
+    double rs = np_sum_rec(0, m, [&](int i) {  // numpy pairwise order for any m (model.py:148)
         double g = gemv_row(P, i, m, [&](int q) { return x[i * P + q]; }, [&](int q) { return b[q < P ? q : P - 1]; });
         return fabs(dsub(y[i], g));
     });

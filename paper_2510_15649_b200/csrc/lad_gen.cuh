@@ -4,14 +4,116 @@
 // §8d), and at config 4 scale (64M problems, ~127 GB of fp64 X) the inputs
 // must be generated where they are solved.  Problem i of a config draws from a
 // counter-based Philox4x32-10 stream keyed by (seed, i), so any index shard is
-// reproducible on any GPU without communication.  Parity tests copy the exact
-// generated bytes back to the host for the CPU oracle.
+// reproducible on any GPU without communication.
+//
+// Host reproducibility: every floating-point operation below is a single IEEE
+// operation (+, -, *, /, sqrt, explicit fma; the library builds with
+// -fmad=false so nothing is contracted), and the transcendentals (log, sinpi,
+// cospi, tan) are this file's own polynomials instead of libdevice's.  A plain
+// C restatement (oracle/gen_host.c, built with -ffp-contract=off) therefore
+// produces the same bytes on the CPU, which is how the CPU reference arm and
+// the reference-held goldens (tests/golden/bench_cfg*.npz) see exactly the
+// problems the GPU solves without loading this library.
 #pragma once
 #include <cuda_runtime.h>
-#include <math_constants.h>
 #include <stdint.h>
 
 namespace lad {
+namespace genmath {
+
+// natural log for finite x > 0 (normal range): x = 2^e m, m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(s), s = (m - 1)/(m + 1), atanh series to s^25 (|s| <= 0.1716)
+__device__ __forceinline__ double log_pos(double x)
+{
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    int e = (int)(b >> 52) - 1023;
+    double m = __longlong_as_double((long long)((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+    if (m > 0x1.6a09e667f3bcdp+0) {
+        m = m * 0.5;
+        e += 1;
+    }
+    double f = m - 1.0;
+    double s = f / (2.0 + f);
+    double z = s * s;
+    double r = 0x1.47ae147ae147bp-5;
+    r = fma(r, z, 0x1.642c8590b2164p-5);
+    r = fma(r, z, 0x1.8618618618618p-5);
+    r = fma(r, z, 0x1.af286bca1af28p-5);
+    r = fma(r, z, 0x1.e1e1e1e1e1e1ep-5);
+    r = fma(r, z, 0x1.1111111111111p-4);
+    r = fma(r, z, 0x1.3b13b13b13b14p-4);
+    r = fma(r, z, 0x1.745d1745d1746p-4);
+    r = fma(r, z, 0x1.c71c71c71c71cp-4);
+    r = fma(r, z, 0x1.2492492492492p-3);
+    r = fma(r, z, 0x1.999999999999ap-3);
+    r = fma(r, z, 0x1.5555555555555p-2);
+    r = r * z;
+    double t = 2.0 * s;
+    double lm = fma(t, r, t);
+    double de = (double)e;
+    return de * 0x1.62e42fee00000p-1 + (de * 0x1.a39ef35793c76p-33 + lm);  // ln2 split (hi has 32 bits)
+}
+
+// sin(pi r), cos(pi r) for |r| <= 1/4: Taylor polynomials in r^2 (|pi r| <= 0.7854)
+__device__ __forceinline__ double sinpi_red(double r)
+{
+    double z = r * r;
+    double q = -0x1.8a404211f9547p-26;
+    q = fma(q, z, 0x1.aaec32af93359p-21);
+    q = fma(q, z, -0x1.6fadb9f155744p-16);
+    q = fma(q, z, 0x1.e8f434d018d63p-12);
+    q = fma(q, z, -0x1.e3074fde8871fp-8);
+    q = fma(q, z, 0x1.50783487ee782p-4);
+    q = fma(q, z, -0x1.32d2cce62bd86p-1);
+    q = fma(q, z, 0x1.466bc6775aae2p+1);
+    q = fma(q, z, -0x1.4abbce625be53p+2);
+    q = fma(q, z, 0x1.921fb54442d18p+1);
+    return r * q;
+}
+
+__device__ __forceinline__ double cospi_red(double r)
+{
+    double z = r * r;
+    double q = 0x1.ef6e308d6d1c4p-29;
+    q = fma(q, z, -0x1.2a0c591af8314p-23);
+    q = fma(q, z, 0x1.20c62c2f2d7f5p-18);
+    q = fma(q, z, -0x1.b6e24f44b128fp-14);
+    q = fma(q, z, 0x1.f9d38a3763cc3p-10);
+    q = fma(q, z, -0x1.a6d1f2a204a8cp-6);
+    q = fma(q, z, 0x1.e1f506891babbp-3);
+    q = fma(q, z, -0x1.55d3c7e3cbffap+0);
+    q = fma(q, z, 0x1.03c1f081b5ac4p+2);
+    q = fma(q, z, -0x1.3bd3cc9be45dep+2);
+    return fma(q, z, 1.0);
+}
+
+// cos(pi x) for x in [0, 2): quarter-turn reduction (exact: x is a multiple of 2^-52)
+__device__ __forceinline__ double cospi_0_2(double x)
+{
+    double q = rint(x * 2.0);
+    double r = x - q * 0.5;
+    switch (((int)q) & 3) {
+    case 0: return cospi_red(r);
+    case 1: return -sinpi_red(r);
+    case 2: return -cospi_red(r);
+    default: return sinpi_red(r);
+    }
+}
+
+// tan(pi w) for w in (-1/2, 1/2), w != +-1/2
+__device__ __forceinline__ double tanpi_open(double w)
+{
+    double a = fabs(w);
+    double t;
+    if (a <= 0.25) t = sinpi_red(a) / cospi_red(a);
+    else {
+        double v = 0.5 - a;  // exact (Sterbenz)
+        t = cospi_red(v) / sinpi_red(v);
+    }
+    return w < 0.0 ? -t : t;
+}
+
+}  // namespace genmath
 
 struct Philox {
     uint32_t k0, k1;
@@ -56,25 +158,29 @@ struct Philox {
         uint64_t v = ((hi << 32) | lo) >> 11;
         return (double)v * 0x1.0p-53;
     }
-    // (0, 1)
+    // (0, 1): an odd 53-bit integer times 2^-53 (exact; never 0, 1/2 or 1)
     __device__ __forceinline__ double uniform_open()
     {
         uint64_t hi = u32(), lo = u32();
-        uint64_t v = ((hi << 32) | lo) >> 11;
-        return ((double)v + 0.5) * 0x1.0p-53;
+        uint64_t v = ((((hi << 32) | lo) >> 12) << 1) | 1u;
+        return (double)v * 0x1.0p-53;
     }
+    // Box-Muller (cosine branch)
     __device__ __forceinline__ double normal()
     {
         double u1 = uniform_open(), u2 = uniform();
-        return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+        return sqrt(-2.0 * genmath::log_pos(u1)) * genmath::cospi_0_2(2.0 * u2);
     }
     __device__ __forceinline__ double laplace(double scale)
     {
-        double u = uniform_open() - 0.5;
+        double u = uniform_open() - 0.5;  // exact, nonzero
         double s = u < 0 ? -1.0 : 1.0;
-        return -scale * s * log1p(-2.0 * fabs(u));
+        return -scale * s * genmath::log_pos(1.0 - 2.0 * fabs(u));
     }
-    __device__ __forceinline__ double cauchy(double scale) { return scale * tan(CUDART_PI * (uniform_open() - 0.5)); }
+    __device__ __forceinline__ double cauchy(double scale)
+    {
+        return scale * genmath::tanpi_open(uniform_open() - 0.5);
+    }
     __device__ __forceinline__ double student_t3()
     {
         double z = normal();

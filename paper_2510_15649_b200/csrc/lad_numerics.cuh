@@ -94,6 +94,50 @@ __device__ __forceinline__ auto np_sum(int n, F f) -> decltype(f(0))
     return res;
 }
 
+// numpy pairwise_sum of f(off), ..., f(off + n - 1) (loops_utils.h.src), any n:
+// blocked below 129 terms, recursion on halves split at a multiple of 8 above
+// (iterative post-order walk of numpy's recursion tree: no device recursion / stack growth)
+template <typename F>
+__device__ double np_sum_rec(int off, int n, F f)
+{
+    if (n <= 128) return np_sum(n, [&](int i) { return f(off + i); });
+    int fo[12], fn[12], fs[12];
+    double fl[12];
+    int sp = 0;
+    fo[0] = off;
+    fn[0] = n;
+    fs[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        const int o = fo[sp], m = fn[sp];
+        if (m <= 128) {
+            ret = np_sum(m, [&](int i) { return f(o + i); });
+            --sp;
+            continue;
+        }
+        int m2 = m / 2;
+        m2 -= m2 % 8;
+        if (fs[sp] == 0) {  // left half first
+            fs[sp] = 1;
+            ++sp;
+            fo[sp] = o;
+            fn[sp] = m2;
+            fs[sp] = 0;
+        } else if (fs[sp] == 1) {  // then the right half
+            fl[sp] = ret;
+            fs[sp] = 2;
+            ++sp;
+            fo[sp] = o + m2;
+            fn[sp] = m - m2;
+            fs[sp] = 0;
+        } else {
+            ret = dadd(fl[sp], ret);
+            --sp;
+        }
+    }
+    return ret;
+}
+
 // Same tree with fully unrolled loops for a compile-time length N.
 template <int N, typename F>
 __device__ __forceinline__ auto np_sum_c(F f) -> decltype(f(0))
