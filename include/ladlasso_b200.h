@@ -24,7 +24,10 @@
  * message available from lad_last_error() (thread-local).  Per-problem failures
  * never abort a batch; they are reported in `status`:
  *   0 ok, 1 unbounded direction (UnboundedDirectionError, linesearch.py:266),
- *   2 invalid input (InvalidInputError: non-finite data or lambda < 0).
+ *   2 invalid input (InvalidInputError: non-finite data, lambda < 0, bad bracket),
+ *   3 scratch capacity exceeded (the search recorded more curve points than
+ *     prm->seen_capacity allows; re-run the problem with a larger capacity --
+ *     the Python API does this automatically).
  * Non-convergence is not an error (converged = 0), as in the reference.
  */
 #ifndef LADLASSO_B200_H
@@ -57,6 +60,9 @@ typedef struct lad_locus_params {
     double inner_sweep_tol;       /* 1e-10 */
     int32_t inner_max_sweeps;     /* 500 */
     double lambda_floor;          /* 1e-9 */
+    int32_t seen_capacity;        /* curve points one evaluator keeps for the nearest-point warm start
+                                     (locus.py:188-191): 0 = automatic (bounded by the outer tolerance,
+                                     with slack); a problem that needs more ends with status 3 */
 } lad_locus_params;
 
 /* Per-problem outputs (SolveResult fields, model.py:113-133, plus work counters). */
@@ -105,6 +111,19 @@ int lad_locus_solve_f64(const double *X, const double *Y, const double *lam, con
 int lad_locus_solve_host_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
                              int64_t Bd, int64_t B, int32_t n, int32_t p, const lad_locus_params *prm,
                              const lad_locus_out *out, void *stream);
+
+/* solve_locus with a per-problem LocusConfig.initial_bracket (locus.py:56, consumed at :227 and
+ * :364-365): brackets (B, 2) = (lo, hi) per problem (device pointer; the _host variant takes host
+ * pointers like lad_locus_solve_host_f64).  A bracket that is not finite with lo < hi marks its
+ * problem invalid (status 2), as Bracket() raises InvalidInputError (linesearch.py:85-89).
+ * prm->has_bracket is ignored.  Used by the warm-started lambda path (bench.py --warm). */
+int lad_locus_solve_bracketed_f64(const double *X, const double *Y, const double *lam, const int64_t *data_index,
+                                  int64_t Bd, int64_t B, int32_t n, int32_t p, const double *brackets,
+                                  const lad_locus_params *prm, const lad_locus_out *out, void *stream);
+int lad_locus_solve_bracketed_host_f64(const double *X, const double *Y, const double *lam,
+                                       const int64_t *data_index, int64_t Bd, int64_t B, int32_t n, int32_t p,
+                                       const double *brackets, const lad_locus_params *prm,
+                                       const lad_locus_out *out, void *stream);
 
 /* Batched ccd_descend from `start` (B, p); frozen (B,) axis or -1 (NULL = none). */
 int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,

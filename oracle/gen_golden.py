@@ -422,6 +422,51 @@ def gen_bench(pool, quick=False):
     _locus_fixture(pool, "bench_cfg4", X, Y, lam, ("ternary",), extra=dict(beta_true=bt, seed=15653, first=0))
 
 
+def _warm_task(args):
+    """One dataset's warm lambda path on the reference (the rule of paper_2510_15649_b200/path.py)."""
+    L = _ref()
+    import ladlasso.locus as LL
+    from ladlasso.linesearch import Bracket
+    from ladlasso.model import Dataset, ProblemSpec
+
+    x, y, lams, variant = args
+    res = [None] * len(lams)
+    prev = None
+    for k in np.argsort(-np.asarray(lams), kind="stable"):
+        br = None
+        if prev is not None:
+            R = max(1.0, 2.0 * float(np.abs(prev).max()))
+            br = Bracket(-R, R)
+        r = LL.solve_locus(ProblemSpec(Dataset(x, y), float(lams[k])),
+                           LL.LocusConfig(outer_search=variant, initial_bracket=br))
+        res[k] = (r.beta.beta.copy(), r.objective, r.iterations, r.objective_evals, r.converged)
+        prev = r.beta.beta
+    return res
+
+
+def gen_warm(pool):
+    """The warm-started lambda path (bench.py --warm) on bench config-2 datasets, both variants."""
+    import oracle as O
+
+    O.build()
+    firsts = [0, 1, 2, 63 * 16384 + 5]
+    X = np.concatenate([O.generate(2, 1, 15651, f)[0] for f in firsts])
+    Y = np.concatenate([O.generate(2, 1, 15651, f)[1] for f in firsts])
+    lams = configs_np.LAMBDA_GRID
+    out = dict(x=X, y=Y, lambdas=lams, dataset_index=np.asarray(firsts), seed=15651)
+    for v in ("ternary", "quadrature"):
+        t0 = time.time()
+        rs = pool.map(_warm_task, [(X[b], Y[b], lams, v) for b in range(len(firsts))], chunksize=1)
+        out[f"{v}_beta"] = np.array([[q[0] for q in r] for r in rs])
+        out[f"{v}_objective"] = np.array([[q[1] for q in r] for r in rs])
+        out[f"{v}_iterations"] = np.array([[q[2] for q in r] for r in rs])
+        out[f"{v}_objective_evals"] = np.array([[q[3] for q in r] for r in rs])
+        out[f"{v}_converged"] = np.array([[q[4] for q in r] for r in rs])
+        print(f"  warm {v}: {len(firsts)} datasets x {len(lams)} lambdas in {time.time() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(GOLDEN, "warm_path.npz"), **out)
+    print("warm_path.npz", flush=True)
+
+
 def _objective_task(args):
     _ref()
     from ladlasso.model import Coefficients, Dataset, ProblemSpec, evaluate_objective
@@ -707,7 +752,8 @@ def main():
         for name, fn in (("kat", gen_kat), ("ccd", gen_ccd), ("acceptance", gen_acceptance),
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
                          ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp), ("large", gen_large),
-                         ("bench", lambda p: gen_bench(p, a.quick)), ("objective", gen_objective)):
+                         ("bench", lambda p: gen_bench(p, a.quick)), ("objective", gen_objective),
+                         ("warm", gen_warm)):
             if only is None or name in only:
                 fn(pool)
 

@@ -842,6 +842,7 @@ typedef struct {
     long long *descents, *steps;
     long long next;
     pthread_mutex_t mu;
+    const double *brackets; /* (B, 2) per-problem initial_bracket or NULL */
 } orc_batch;
 
 static void *batch_worker(void *arg)
@@ -869,7 +870,25 @@ static void *batch_worker(void *arg)
         }
         P.lam = lraw > bt->lam_floor ? lraw : bt->lam_floor;
         orc_locus_result r;
-        solve_locus(&P, bt->prm, &r);
+        if (bt->brackets) { /* LocusConfig(initial_bracket=Bracket(lo, hi)) per problem (locus.py:56) */
+            orc_locus_params prm = *bt->prm;
+            prm.has_bracket = 1;
+            prm.bracket_lo = bt->brackets[2 * b];
+            prm.bracket_hi = bt->brackets[2 * b + 1];
+            if (!(isfinite(prm.bracket_lo) && isfinite(prm.bracket_hi) && prm.bracket_lo < prm.bracket_hi)) {
+                /* Bracket() raises InvalidInputError (linesearch.py:85-89): status 2 */
+                for (int j = 0; j < bt->d; ++j) bt->beta[(size_t)b * bt->d + j] = NAN;
+                bt->obj[b] = NAN;
+                bt->iters[b] = bt->evals[b] = bt->conv[b] = 0;
+                bt->status[b] = 2;
+                if (bt->descents) bt->descents[b] = 0;
+                if (bt->steps) bt->steps[b] = 0;
+                continue;
+            }
+            solve_locus(&P, &prm, &r);
+        } else {
+            solve_locus(&P, bt->prm, &r);
+        }
         memcpy(bt->beta + (size_t)b * bt->d, r.beta, sizeof(double) * bt->d);
         bt->obj[b] = r.objective;
         bt->iters[b] = r.iterations;
@@ -901,6 +920,18 @@ int orc_solve_locus_batch(const double *X, const double *Y, const double *L, lon
     if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
     orc_batch bt = {X, Y, L, NULL, NULL, NULL, B, m, d, lam_floor, prm, beta, obj, iters, evals, conv, status,
                     descents, steps, 0};
+    return run_batch(&bt, nthreads);
+}
+
+int orc_solve_locus_batch_brackets(const double *X, const double *Y, const double *L, long long B, int m, int d,
+                                   double lam_floor, const orc_locus_params *prm, const double *brackets,
+                                   int nthreads, double *beta, double *obj, int *iters, int *evals, int *conv,
+                                   int *status, long long *descents, long long *steps)
+{
+    if (m < 1 || d < 1 || m > ORC_MAX_M || d > ORC_MAX_D) return -1;
+    orc_batch bt = {X, Y, L, NULL, NULL, NULL, B, m, d, lam_floor, prm, beta, obj, iters, evals, conv, status,
+                    descents, steps, 0};
+    bt.brackets = brackets;
     return run_batch(&bt, nthreads);
 }
 

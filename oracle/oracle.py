@@ -96,6 +96,10 @@ def lib():
         L.orc_solve_locus_batch.restype = C.c_int
         L.orc_solve_locus_batch.argtypes = [dp, dp, dp, C.c_longlong, C.c_int, C.c_int, C.c_double,
                                             C.POINTER(LocusParams), C.c_int, dp, dp, ip, ip, ip, ip, lp, lp]
+        L.orc_solve_locus_batch_brackets.restype = C.c_int
+        L.orc_solve_locus_batch_brackets.argtypes = [dp, dp, dp, C.c_longlong, C.c_int, C.c_int, C.c_double,
+                                                     C.POINTER(LocusParams), dp, C.c_int, dp, dp, ip, ip, ip, ip, lp,
+                                                     lp]
         L.orc_solve_linear_system.restype = C.c_int
         L.orc_solve_linear_system.argtypes = [dp, dp, C.c_int, C.c_double, dp]
         L.orc_candidate_count.restype = C.c_longlong
@@ -292,9 +296,10 @@ def solve_locus(x, y, lam_eff, **kw) -> LocusResult:
     return LocusResult(beta, obj.value, it.value, ev.value, bool(cv.value), stt.value, dsc.value, stp.value)
 
 
-def solve_locus_batch(X, Y, L, lambda_floor=1e-9, nthreads=None, **kw):
+def solve_locus_batch(X, Y, L, lambda_floor=1e-9, nthreads=None, brackets=None, **kw):
     """Batched oracle solve over host threads; X (B,m,d), Y (B,m), L (B,) raw lambdas.
-    float32 X/Y select the fp32 mode (then L is taken as float32 too)."""
+    float32 X/Y select the fp32 mode (then L is taken as float32 too).  brackets (B, 2):
+    a per-problem LocusConfig.initial_bracket (fp64 only)."""
     f32 = _is_f32(X, Y)
     cv_ = _f if f32 else _d
     X, pX = cv_(X)
@@ -313,6 +318,19 @@ def solve_locus_batch(X, Y, L, lambda_floor=1e-9, nthreads=None, **kw):
     stp = np.empty(B, np.int64)
     ip = C.POINTER(C.c_int)
     lp = C.POINTER(C.c_longlong)
+    if brackets is not None:
+        if f32:
+            raise ValueError("per-problem brackets: fp64 only")
+        bk, pk = _d(np.asarray(brackets, dtype=np.float64).reshape(B, 2))
+        rc = lib().orc_solve_locus_batch_brackets(pX, pY, pL, B, m, d, lambda_floor, C.byref(prm), pk, nthreads,
+                                                  beta.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  obj.ctypes.data_as(C.POINTER(C.c_double)), it.ctypes.data_as(ip),
+                                                  ev.ctypes.data_as(ip), cv.ctypes.data_as(ip), stt.ctypes.data_as(ip),
+                                                  dsc.ctypes.data_as(lp), stp.ctypes.data_as(lp))
+        if rc:
+            raise ValueError("problem shape outside oracle limits")
+        return dict(beta=beta, objective=obj, iterations=it, objective_evals=ev, converged=cv.astype(bool),
+                    status=stt, descents=dsc, steps=stp)
     fn = lib().orc_solve_locus_batch_f32 if f32 else lib().orc_solve_locus_batch
     rc = fn(pX, pY, pL, B, m, d, lambda_floor, C.byref(prm), nthreads,
                                      beta.ctypes.data_as(C.POINTER(C.c_double)),
@@ -392,3 +410,27 @@ def config3_dataset(seed: int = 15649 + 3):
     """The one n=30, p=5 dataset of config 3 (config-0 problem 0 under config 3's seed)."""
     X, Y, _ = generate(0, 1, seed)
     return X[0], Y[0]
+
+
+# ---- the warm-started lambda path (paper_2510_15649_b200/path.py defines the rule) ----
+
+def solve_warm_path(X, Y, lambdas, outer_search="ternary", nthreads=None):
+    """Replay of path.solve_lambda_path_batched(warm=True): largest lambda first with the
+    default bracket, then Bracket(-R, R), R = max(1, 2 max_j |beta_prev_j|) (1 after a failed
+    solve); every stage a reference solve_locus call with initial_bracket.  Returns arrays
+    shaped (B, L, ...) in the order of `lambdas`."""
+    lam = np.asarray(lambdas, dtype=np.float64).reshape(-1)
+    B, nl = X.shape[0], lam.size
+    out, prev = {}, None
+    for k in np.argsort(-lam, kind="stable"):
+        L = np.full(B, float(lam[k]))
+        if prev is None:
+            r = solve_locus_batch(X, Y, L, nthreads=nthreads, outer_search=outer_search)
+        else:
+            R = np.maximum(1.0, 2.0 * np.abs(prev["beta"]).max(axis=1))
+            R = np.where(prev["status"] == 0, R, 1.0)
+            r = solve_locus_batch(X, Y, L, nthreads=nthreads, outer_search=outer_search,
+                                  brackets=np.stack([-R, R], axis=1))
+        out[k] = r
+        prev = r
+    return {f: np.stack([out[k][f] for k in range(nl)], axis=1) for f in out[0]}

@@ -22,6 +22,7 @@ from .solver import (validate_result, BatchedSolveResult, Coefficients, Dataset,
                      solve_locus_batched)
 from .lp import (LpStandardForm, SimplexConfig, SimplexSolution, dump_lp, formulate, simplex_minimize, simplex_solve,
                  solve_lp, solve_lp_batched)
+from .path import solve_lambda_path_batched
 from .synth import GenSpec, generate, read_dataset_csv, write_dataset_csv
 from .curve import (LocusPoint, axes_by_influence, default_bracket, default_outer_axis, locus_value,
                     perturb_restart, sample_locus, sample_locus_batched)
@@ -37,5 +38,5 @@ __all__ = [
     "default_bracket", "default_outer_axis", "locus_value", "perturb_restart", "sample_locus", "sample_locus_batched",
     "SimplexConfig", "SimplexSolution", "SimplexError", "solve_lp", "solve_lp_batched",
     "LpStandardForm", "dump_lp", "formulate", "simplex_minimize", "simplex_solve", "GenSpec", "generate",
-    "read_dataset_csv", "write_dataset_csv", "validate_result",
+    "read_dataset_csv", "write_dataset_csv", "validate_result", "solve_lambda_path_batched",
 ]

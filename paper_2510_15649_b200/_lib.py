@@ -33,6 +33,8 @@ SYMBOLS = (
     "lad_fp32_peak_tflops",
     "lad_axiswise_minimum_f64",
     "lad_lp_solve_f64",
+    "lad_locus_solve_bracketed_f64",
+    "lad_locus_solve_bracketed_host_f64",
 )
 
 LAD_OK = 0
@@ -40,6 +42,7 @@ LAD_E_INVALID = -1
 LAD_E_TOO_LARGE = -2
 LAD_E_CUDA = -3
 LAD_E_UNSUPPORTED = -4
+STATUS_SCRATCH = 3  # per-problem: the evaluator's curve-point list outgrew prm.seen_capacity
 
 KERNEL_AUTO = 0
 KERNEL_THREAD = 1
@@ -72,6 +75,7 @@ class LocusParams(C.Structure):
         ("inner_sweep_tol", C.c_double),
         ("inner_max_sweeps", C.c_int32),
         ("lambda_floor", C.c_double),
+        ("seen_capacity", C.c_int32),
     ]
 
 
@@ -119,6 +123,9 @@ def load(build_if_missing: bool = False):
                                       vp]
     L.lad_locus_solve_host_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, C.POINTER(LocusParams),
                                            C.POINTER(LocusOut), vp]
+    L.lad_locus_solve_bracketed_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, vp, C.POINTER(LocusParams),
+                                                C.POINTER(LocusOut), vp]
+    L.lad_locus_solve_bracketed_host_f64.argtypes = L.lad_locus_solve_bracketed_f64.argtypes
     L.lad_fp64_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
     L.lad_fp32_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
     L.lad_locus_solve_f32.argtypes = L.lad_locus_solve_f64.argtypes

@@ -40,6 +40,7 @@ struct LocusParamsDev {
     double inner_sweep_tol;
     int32_t inner_max_sweeps;
     double lambda_floor;
+    int32_t seen_capacity;
 };
 
 enum : int { MODE_LOCUS = 0, MODE_DESCENT = 1 };
@@ -70,7 +71,8 @@ struct LocusArgs {
     int64_t *steps;         // may be null
     // scratch
     double *seen;           // per lane slot: seen_cap * (1 + PMAX) doubles
-    int seen_cap;
+    int seen_cap;           // curve points kept per evaluator; more -> status 3 (see seen_append)
+    const double *brackets; // (B, 2) per-problem initial_bracket (lo, hi), or null (LocusConfig's / default)
     unsigned long long *counter;
     // axis-parallel mode (AXIS_SEARCH: item = problem * p + axis rank)
     int axis_mode;
@@ -134,7 +136,7 @@ struct Ctl {
     int warm_idx;
     Point<PMAX> pt;
     // evaluator (_CurveEvaluator)
-    int axis, nseen, ev_calls, ev_failures, has_best;
+    int axis, nseen, ev_calls, ev_failures, has_best, seen_over;
     Point<PMAX> ev_best;
     double fast_tol, inner_tol, margin_scale;
     int fast_sweeps, inner_sweeps, economy;
@@ -225,7 +227,11 @@ __device__ __forceinline__ void seen_append(const LocusArgs &A, double *seen, Ct
 {
     if (seen == nullptr) return;
     int k = C.nseen;
-    if (leader && k < A.seen_cap) {
+    if (k >= A.seen_cap) {  // capacity exceeded: the nearest-point scan would be incomplete, so the
+        C.seen_over = 1;    // problem ends with status 3 instead of a silently different warm start
+        return;
+    }
+    if (leader) {
         seen[k] = P.t;
         double *sb = seen + A.seen_cap + (size_t)k * PMAX;
         for (int j = 0; j < p; ++j) sb[j] = P.beta[j];
@@ -403,6 +409,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             C.D = 0;
             C.S = 0;
             C.replay = 0;
+            C.seen_over = 0;
             if (got == 0) continue;  // invalid problem: status written, fetch the next one
             const int64_t pr = C.prob;
             if (A.mode == MODE_DESCENT) {
@@ -433,7 +440,16 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                 }
                 C.naxes = p;
             }
-            if (A.prm.has_bracket) {
+            if (A.brackets) {  // per-problem initial_bracket (Bracket validation, linesearch.py:85-89)
+                const double blo = A.brackets[2 * pr], bhi = A.brackets[2 * pr + 1];
+                if (!(isfinite(blo) && isfinite(bhi) && blo < bhi)) {
+                    if (acc.leader()) write_invalid<PMAX>(A, pr, p);
+                    C.pc = PC_FETCH;
+                    continue;
+                }
+                C.R_lo = blo;
+                C.R_hi = bhi;
+            } else if (A.prm.has_bracket) {
                 C.R_lo = A.prm.bracket_lo;
                 C.R_hi = A.prm.bracket_hi;
             } else {
@@ -471,6 +487,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             C.ev_calls = (int)__ldcg(res + 4 + PMAX);
             C.ev_failures = (int)__ldcg(res + 5 + PMAX);
             C.oconv = (int)__ldcg(res + 6 + PMAX);
+            C.seen_over |= (int)__ldcg(res + 9 + PMAX);
             C.D += (int)__ldcg(res + 7 + PMAX);
             C.S += (long long)__ldcg(res + 8 + PMAX);
             if (C.oconv < 0) {  // this axis' bracket expansion failed: raise here, as the serial scan does
@@ -500,6 +517,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
             C.confirmations = 0;
             C.D = 0;  // the replay adds every axis' D and S
             C.S = 0;
+            C.seen_over = 0;
             C.pc = PC_FINISH_AXES;
             acc.sync();
             break;
@@ -540,6 +558,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                         res[6 + PMAX] = -1.0;
                         res[7 + PMAX] = C.D;
                         res[8 + PMAX] = (double)C.S;
+                        res[9 + PMAX] = C.seen_over;
                     }
                     C.pc = PC_AXIS_COUNT;
                     break;
@@ -639,6 +658,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                     res[6 + PMAX] = C.oconv;
                     res[7 + PMAX] = C.D;
                     res[8 + PMAX] = (double)C.S;
+                    res[9 + PMAX] = C.seen_over;
                 }
                 C.pc = PC_AXIS_COUNT;
                 break;
@@ -809,6 +829,18 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
         case PC_POLISH_AFTER: {
             int64_t pr = C.prob;
             bool use_pol = C.res_obj <= C.best.value;
+            if (C.seen_over) {  // scratch capacity exceeded (see seen_append): status 3, counters kept
+                if (acc.leader()) {
+                    write_invalid<PMAX>(A, pr, p);
+                    A.status[pr] = 3;
+                    A.iterations[pr] = C.rounds;
+                    A.objective_evals[pr] = C.calls;
+                    if (A.descents) A.descents[pr] = C.D;
+                    if (A.steps) A.steps[pr] = C.S;
+                }
+                C.pc = PC_FETCH;
+                break;
+            }
             if (acc.leader()) {
             for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = use_pol ? C.res_beta[j] : C.best.beta[j];
             A.objective[pr] = use_pol ? C.res_obj : C.best.value;

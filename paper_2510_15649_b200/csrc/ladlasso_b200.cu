@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <string>
 
@@ -61,6 +62,7 @@ extern "C" void lad_default_params(lad_locus_params *prm)
     prm->inner_sweep_tol = 1e-10;
     prm->inner_max_sweeps = 500;
     prm->lambda_floor = 1e-9;
+    prm->seen_capacity = 0;
 }
 
 static_assert(sizeof(lad_locus_params) == sizeof(lad::LocusParamsDev), "params layout");
@@ -159,22 +161,38 @@ cudaError_t device_init()
     return cudaSuccess;
 }
 
+// Curve points one _CurveEvaluator can record (locus.py:188-191, :210-212, :278-288): the bracket
+// expansion (2 + 3 per iteration, at most 60: linesearch.py:247-268), the outer rounds (2 probes per
+// ternary round, `probes` per quadrature round) and the final mid probe; a refine evaluator holds
+// 1 + fan + 64.  The outer rounds are bounded by the tolerance (ternary shrinks the bracket to 2/3
+// per round, quadrature to 2/(probes+1)) plus 32 rounds of slack, not by outer_max_iterations: a
+// huge max_iterations costs nothing unless a search really stalls, and a search that outgrows the
+// list ends with status 3 (the host API re-runs such problems with prm->seen_capacity = the worst
+// case, worst_case_seen_capacity) instead of silently truncating the nearest-point scan.
+long long worst_case_seen(const lad_locus_params *prm)
+{
+    long long outer = prm->outer_search == LAD_OUTER_TERNARY ? 2LL * prm->outer_max_iterations
+                                                             : (long long)prm->outer_probes * prm->outer_max_iterations;
+    return std::max(2 + 3 * 60 + outer + 1, 1LL + 12 + 64);
+}
+
 int seen_capacity(const lad_locus_params *prm, int p)
 {
-    if (p <= 2) return 0;
-    long long outer = prm->outer_search == LAD_OUTER_TERNARY
-                          ? 2 + 2LL * prm->outer_max_iterations
-                          : 2 + (long long)prm->outer_probes * prm->outer_max_iterations;
-    long long axis = 2 + 3 * 60 + outer;
-    long long refine = 1 + 12 + 64;
-    long long cap = std::max(axis, refine);
-    return (int)std::min<long long>(cap, 1 << 20);
+    if (p <= 2) return 0;  // no warm starts below d = 3 (locus.py:199-202)
+    if (prm->seen_capacity > 0) return (int)std::min<long long>(prm->seen_capacity, worst_case_seen(prm));
+    const double shrink = prm->outer_search == LAD_OUTER_TERNARY ? 2.0 / 3.0 : 2.0 / (prm->outer_probes + 1.0);
+    long long rounds = (long long)std::ceil(std::log(prm->outer_tolerance) / std::log(shrink));
+    rounds = std::max(0LL, rounds) + 32;
+    rounds = std::min<long long>(rounds, prm->outer_max_iterations);
+    const long long per_round = prm->outer_search == LAD_OUTER_TERNARY ? 2 : prm->outer_probes;
+    return (int)std::min(std::max(2 + 3 * 60 + per_round * rounds + 1, 1LL + 12 + 64), worst_case_seen(prm));
 }
 
 // X, Y, lam are double* (f32 == false) or float* (f32 == true)
 int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data_index, int64_t Bd, int64_t B, int n, int p,
               const lad_locus_params *prm, const lad_locus_out *out, cudaStream_t st, int mode, const double *start,
-              const int32_t *frozen, double desc_tol, int desc_sweeps, bool f32 = false)
+              const int32_t *frozen, double desc_tol, int desc_sweeps, bool f32 = false,
+              const double *brackets = nullptr)
 {
     if (B < 0 || n < 1 || p < 1) return fail(LAD_E_INVALID, "need B >= 0, n >= 1, p >= 1 (got %lld, %d, %d)", (long long)B, n, p);
     if (B == 0) return LAD_OK;
@@ -189,7 +207,8 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     if (prm->inner_sweep_tol <= 0) return fail(LAD_E_INVALID, "sweep_tolerance must be positive");
     if (prm->inner_max_sweeps < 1) return fail(LAD_E_INVALID, "max_sweeps must be at least 1");
     if (prm->outer_axis >= p) return fail(LAD_E_INVALID, "outer_axis %d out of range for d=%d", prm->outer_axis, p);
-    if (prm->has_bracket && !(prm->bracket_lo < prm->bracket_hi))
+    if (prm->seen_capacity < 0) return fail(LAD_E_INVALID, "seen_capacity must be >= 0");
+    if (!brackets && prm->has_bracket && !(prm->bracket_lo < prm->bracket_hi))
         return fail(LAD_E_INVALID, "bracket needs lo < hi");
     if (!(prm->lambda_floor > 0)) return fail(LAD_E_INVALID, "lambda_floor must be finite and > 0");
     Variant v;
@@ -246,6 +265,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     A.descents = out->descents;
     A.steps = out->steps;
     A.seen_cap = mode == lad::MODE_LOCUS ? seen_capacity(prm, p) : 0;
+    A.brackets = mode == lad::MODE_LOCUS ? brackets : nullptr;
     size_t seen_bytes = (size_t)slots * A.seen_cap * (1 + v.pmax) * sizeof(double);
     A.axis_stride = v.pmax + 10;
     size_t axis_bytes = axis_par ? (size_t)B * p * A.axis_stride * sizeof(double) : 0;
@@ -312,6 +332,21 @@ extern "C" int lad_locus_solve_f64(const double *X, const double *Y, const doubl
                      nullptr, 0.0, 0);
 }
 
+extern "C" int lad_locus_solve_bracketed_f64(const double *X, const double *Y, const double *lam,
+                                             const int64_t *data_index, int64_t Bd, int64_t B, int32_t n, int32_t p,
+                                             const double *brackets, const lad_locus_params *prm,
+                                             const lad_locus_out *out, void *stream)
+{
+    lad_locus_params def;
+    if (!prm) {
+        lad_default_params(&def);
+        prm = &def;
+    }
+    if (!brackets && B > 0) return fail(LAD_E_INVALID, "brackets must be non-null");
+    return run_locus(X, Y, lam, data_index, Bd, B, n, p, prm, out, (cudaStream_t)stream, lad::MODE_LOCUS, nullptr,
+                     nullptr, 0.0, 0, false, brackets);
+}
+
 extern "C" int lad_ccd_descend_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n,
                                    int32_t p, const double *start, const int32_t *frozen, double sweep_tolerance,
                                    int32_t max_sweeps, double lambda_floor, const lad_locus_out *out, void *stream)
@@ -355,7 +390,8 @@ extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *
 
 template <typename T>
 static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t *data_index, int64_t Bd, int64_t B,
-                            int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream)
+                            int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream,
+                            const double *brackets = nullptr)
 {
     cudaStream_t st = (cudaStream_t)stream;
     if (B < 0 || Bd < 0) return fail(LAD_E_INVALID, "B < 0");
@@ -365,8 +401,9 @@ static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t 
     const size_t es = sizeof(T);
     size_t bx = (size_t)Bd * n * p * es, by = (size_t)Bd * n * es, bl = (size_t)B * es, bb = (size_t)B * p * 8;
     size_t bi = data_index ? (size_t)B * 8 : 0;
-    size_t total = rup(bx) + rup(by) + rup(bl) + rup(bi) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) + 2 * rup(B) +
-                   rup(B * 4) + rup(B * 8);
+    size_t bk = brackets ? (size_t)B * 16 : 0;
+    size_t total = rup(bx) + rup(by) + rup(bl) + rup(bi) + rup(bk) + rup(bb) + rup(B * 8) + 2 * rup(B * 4) +
+                   2 * rup(B) + rup(B * 4) + rup(B * 8);
     char *d = nullptr;
     CK(cudaMallocAsync((void **)&d, total, st));
     char *q = d;
@@ -377,6 +414,7 @@ static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t 
     };
     T *dX = (T *)take(bx), *dY = (T *)take(by), *dL = (T *)take(bl);
     int64_t *dI = data_index ? (int64_t *)take(bi) : nullptr;
+    double *dK = brackets ? (double *)take(bk) : nullptr;
     lad_locus_out dout;
     dout.beta = (double *)take(bb);
     dout.objective = (double *)take(B * 8);
@@ -392,8 +430,10 @@ static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t 
     if (e == cudaSuccess) e = cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && dI) e = cudaMemcpyAsync(dI, data_index, bi, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && dK) e = cudaMemcpyAsync(dK, brackets, bk, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
         if constexpr (sizeof(T) == 4) rc = lad_locus_solve_f32(dX, dY, dL, dI, Bd, B, n, p, prm, &dout, stream);
+        else if (dK) rc = lad_locus_solve_bracketed_f64(dX, dY, dL, dI, Bd, B, n, p, dK, prm, &dout, stream);
         else rc = lad_locus_solve_f64(dX, dY, dL, dI, Bd, B, n, p, prm, &dout, stream);
     }
     if (e == cudaSuccess && rc == LAD_OK) {
@@ -418,6 +458,15 @@ extern "C" int lad_locus_solve_host_f64(const double *X, const double *Y, const 
                                         const lad_locus_params *prm, const lad_locus_out *out, void *stream)
 {
     return locus_solve_host<double>(X, Y, lam, data_index, Bd, B, n, p, prm, out, stream);
+}
+
+extern "C" int lad_locus_solve_bracketed_host_f64(const double *X, const double *Y, const double *lam,
+                                                  const int64_t *data_index, int64_t Bd, int64_t B, int32_t n,
+                                                  int32_t p, const double *brackets, const lad_locus_params *prm,
+                                                  const lad_locus_out *out, void *stream)
+{
+    if (!brackets && B > 0) return fail(LAD_E_INVALID, "brackets must be non-null");
+    return locus_solve_host<double>(X, Y, lam, data_index, Bd, B, n, p, prm, out, stream, brackets);
 }
 
 extern "C" int lad_locus_solve_host_f32(const float *X, const float *Y, const float *lam, const int64_t *data_index,

@@ -45,11 +45,26 @@ def solve_sharded(X, y, lam, solve, group=None, gather: bool = True):
     local = solve(X[s:e], y[s:e], lam[s:e])
     if not gather or world == 1:
         return s, e, local, (local if world == 1 else None)
-    gathered = {}
+    return s, e, local, gather_results(local, B, group)
+
+
+def gather_results(local: dict, B: int, group=None) -> dict:
+    """All-gather per-problem result arrays (numpy or torch, first axis = the rank's contiguous
+    shard of B problems) into global index order on every rank, as numpy arrays.  With NCCL the
+    buffers go through the current CUDA device; with gloo they stay on the host."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return {k: np.asarray(v.cpu() if torch.is_tensor(v) else v) for k, v in local.items()}
     counts = [shard_range(B, world, r)[1] - shard_range(B, world, r)[0] for r in range(world)]
     cap = max(counts)
+    gathered = {}
     for key, val in local.items():
         t = torch.as_tensor(np.asarray(val.cpu() if torch.is_tensor(val) else val))
+        if t.dtype == torch.bool:
+            t = t.to(torch.uint8)
         dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else t.device
         pad = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype)
         pad[: t.shape[0]] = t
@@ -57,4 +72,4 @@ def solve_sharded(X, y, lam, solve, group=None, gather: bool = True):
         bufs = [torch.empty_like(pad) for _ in range(world)]
         dist.all_gather(bufs, pad, group=group)
         gathered[key] = torch.cat([b[:c].cpu() for b, c in zip(bufs, counts)]).numpy()
-    return s, e, local, gathered
+    return gathered

@@ -28,6 +28,7 @@ from .errors import (DeviceError, DimensionMismatchError, InvalidInputError, Pro
 STATUS_OK = 0
 STATUS_UNBOUNDED = 1
 STATUS_INVALID = 2
+STATUS_SCRATCH = 3
 
 
 def _to_device(a, dev):
@@ -106,7 +107,10 @@ class BatchedSolveResult:
             raise UnboundedDirectionError(f"problem {i}: no interior minimum found after 60 bracket extensions")
         if (st == STATUS_INVALID).any():
             i = int(np.nonzero(st == STATUS_INVALID)[0][0])
-            raise InvalidInputError(f"problem {i}: non-finite data or invalid lambda")
+            raise InvalidInputError(f"problem {i}: non-finite data, invalid lambda or invalid bracket")
+        if (st == STATUS_SCRATCH).any():
+            i = int(np.nonzero(st == STATUS_SCRATCH)[0][0])
+            raise DeviceError(f"problem {i}: curve-point scratch exceeded (re-run with a larger seen_capacity)")
 
 
 def _is_f32(X) -> bool:
@@ -154,17 +158,81 @@ def _validate_device(X, y, lam, nlam=None, f32=False):
     return X.contiguous(), y.contiguous(), lam
 
 
+def _brackets_arg(brackets, B, device=None):
+    """(B, 2) float64 per-problem (lo, hi), numpy for the host path or a CUDA tensor for the device path."""
+    if brackets is None:
+        return None
+    if device is not None:
+        import torch
+
+        b = torch.as_tensor(brackets, device=device).to(torch.float64).reshape(-1, 2).contiguous()
+    else:
+        b = np.ascontiguousarray(np.asarray(brackets, dtype=np.float64).reshape(-1, 2))
+    if b.shape[0] != B:
+        raise DimensionMismatchError(f"brackets has {b.shape[0]} rows for {B} problems")
+    return b
+
+
 def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_floor: float = DEFAULT_LAMBDA_FLOOR,
-                        data_index=None, strict: bool = False, stream=None) -> BatchedSolveResult:
+                        data_index=None, brackets=None, strict: bool = False, stream=None,
+                        seen_capacity: int = 0) -> BatchedSolveResult:
     """Batched ``solve_locus`` (locus.py:300).  Inputs numpy (host) or CUDA torch tensors.
 
     float64 inputs run the reference's arithmetic (bit-exact); a float32 X selects
     the fp32 mode (binary32 descents, binary64 outer search; include/ladlasso_b200.h).
-    Outputs are float64 either way."""
+    ``brackets`` (B, 2): a per-problem ``LocusConfig.initial_bracket`` (fp64 only).
+    Outputs are float64 either way.  Problems whose curve-point scratch overflows
+    (status 3, only for searches that stall far past their tolerance) are re-run with
+    the worst-case capacity on the host path and whenever ``strict`` is set."""
+    res = _solve_locus_once(X, y, lam, cfg, lambda_floor, data_index, brackets, stream, seen_capacity)
+    host = not _is_torch(res.status)
+    if (host or strict) and seen_capacity == 0:
+        st = np.asarray(res.status.cpu() if not host else res.status)
+        redo = np.nonzero(st == STATUS_SCRATCH)[0]
+        if redo.size:
+            res = _rerun_scratch(res, redo, X, y, lam, cfg, lambda_floor, data_index, brackets, stream)
+    if strict:
+        res.raise_for_status()
+    return res
+
+
+def _rerun_scratch(res, redo, X, y, lam, cfg, lambda_floor, data_index, brackets, stream):
+    """Re-solve the status-3 problems with the worst-case curve-point capacity and splice them in."""
+    import torch
+
+    on_dev = _is_torch(X)
+    idx = torch.as_tensor(redo, device=X.device) if on_dev else redo
+    B = res.objective.shape[0]
+    lam_all = lam if (on_dev or np.ndim(lam)) else np.full(B, float(lam))
+    if data_index is not None:
+        di = data_index[idx] if on_dev else np.asarray(data_index)[redo]
+        Xs, ys = X, y
+    else:
+        di = None
+        Xs, ys = X[idx], y[idx]
+    br = None if brackets is None else (brackets[idx] if on_dev else np.asarray(brackets).reshape(-1, 2)[redo])
+    lam_s = lam_all[idx] if on_dev else np.asarray(np.broadcast_to(lam_all, (B,)))[redo]
+    p = X.shape[2]
+    prm = locus_params(cfg if cfg is not None else LocusConfig(), lambda_floor, p)
+    cap = _worst_case_seen(prm)
+    sub = _solve_locus_once(Xs, ys, lam_s, cfg, lambda_floor, di, br, stream, cap)
+    for f in ("beta", "objective", "iterations", "objective_evals", "converged", "status", "descents", "steps"):
+        getattr(res, f)[idx] = getattr(sub, f)
+    return res
+
+
+def _worst_case_seen(prm) -> int:
+    outer = 2 * prm.outer_max_iterations if prm.outer_search == 0 else prm.outer_probes * prm.outer_max_iterations
+    return max(2 + 3 * 60 + outer + 1, 1 + 12 + 64)
+
+
+def _solve_locus_once(X, y, lam, cfg, lambda_floor, data_index, brackets, stream, seen_capacity):
     L = _lib.load()
     cfg = cfg if cfg is not None else LocusConfig()
     solver_id = "locus_ternary" if cfg.outer_search == "ternary" else "locus_quadrature"
     f32 = _is_f32(X)
+    if brackets is not None and f32:
+        raise InvalidInputError("per-problem brackets are implemented for float64 problems")
     if _is_torch(X):
         import torch
 
@@ -174,6 +242,8 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
         Bd, n, p = X.shape
         B = lam.shape[0]
         prm = locus_params(cfg, lambda_floor, p)
+        prm.seen_capacity = int(seen_capacity)
+        br = _brackets_arg(brackets, B, X.device)
         dev = X.device
         beta = torch.empty((B, p), dtype=torch.float64, device=dev)
         obj = torch.empty(B, dtype=torch.float64, device=dev)
@@ -187,42 +257,46 @@ def solve_locus_batched(X, y, lam, cfg: LocusConfig | None = None, *, lambda_flo
                             stt.data_ptr(), dsc.data_ptr(), stp.data_ptr())
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         t0 = time.perf_counter()
-        fn = L.lad_locus_solve_f32 if f32 else L.lad_locus_solve_f64
-        _check(fn(X.data_ptr(), y.data_ptr(), lam.data_ptr(),
-                  data_index.data_ptr() if data_index is not None else None, Bd, B, n, p, C.byref(prm), C.byref(out),
-                  s))
-        res = BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
-    else:
-        X, y, lam0 = _validate_host(X, y, 0.0, f32)
-        Bd, n, p = X.shape
-        if data_index is not None:
-            data_index = np.ascontiguousarray(data_index, dtype=np.int64)
-            if data_index.size and (data_index.min() < 0 or data_index.max() >= Bd):
-                raise InvalidInputError("data_index out of range")
-            B = data_index.shape[0]
+        di = data_index.data_ptr() if data_index is not None else None
+        if br is not None:
+            _check(L.lad_locus_solve_bracketed_f64(X.data_ptr(), y.data_ptr(), lam.data_ptr(), di, Bd, B, n, p,
+                                                   br.data_ptr(), C.byref(prm), C.byref(out), s))
         else:
-            B = Bd
-        ft = np.float32 if f32 else np.float64
-        lam = np.array(np.broadcast_to(np.asarray(lam, dtype=ft), (B,)), dtype=ft)
-        prm = locus_params(cfg, lambda_floor, p)
-        beta = _host_empty((B, p))
-        obj = _host_empty(B)
-        it = _host_empty(B, np.int32)
-        ev = _host_empty(B, np.int32)
-        cv = _host_empty(B, np.uint8)
-        stt = _host_empty(B, np.uint8)
-        dsc = _host_empty(B, np.int32)
-        stp = _host_empty(B, np.int64)
-        out = _lib.LocusOut(*(a.ctypes.data for a in (beta, obj, it, ev, cv, stt, dsc, stp)))
-        t0 = time.perf_counter()
+            fn = L.lad_locus_solve_f32 if f32 else L.lad_locus_solve_f64
+            _check(fn(X.data_ptr(), y.data_ptr(), lam.data_ptr(), di, Bd, B, n, p, C.byref(prm), C.byref(out), s))
+        return BatchedSolveResult(beta, obj, it, ev, cv.bool(), stt, dsc, stp, solver_id, time.perf_counter() - t0)
+    X, y, lam0 = _validate_host(X, y, 0.0, f32)
+    Bd, n, p = X.shape
+    if data_index is not None:
+        data_index = np.ascontiguousarray(data_index, dtype=np.int64)
+        if data_index.size and (data_index.min() < 0 or data_index.max() >= Bd):
+            raise InvalidInputError("data_index out of range")
+        B = data_index.shape[0]
+    else:
+        B = Bd
+    ft = np.float32 if f32 else np.float64
+    lam = np.array(np.broadcast_to(np.asarray(lam, dtype=ft), (B,)), dtype=ft)
+    prm = locus_params(cfg, lambda_floor, p)
+    prm.seen_capacity = int(seen_capacity)
+    br = _brackets_arg(brackets, B)
+    beta = _host_empty((B, p))
+    obj = _host_empty(B)
+    it = _host_empty(B, np.int32)
+    ev = _host_empty(B, np.int32)
+    cv = _host_empty(B, np.uint8)
+    stt = _host_empty(B, np.uint8)
+    dsc = _host_empty(B, np.int32)
+    stp = _host_empty(B, np.int64)
+    out = _lib.LocusOut(*(a.ctypes.data for a in (beta, obj, it, ev, cv, stt, dsc, stp)))
+    t0 = time.perf_counter()
+    di = None if data_index is None else data_index.ctypes.data
+    if br is not None:
+        _check(L.lad_locus_solve_bracketed_host_f64(X.ctypes.data, y.ctypes.data, lam.ctypes.data, di, Bd, B, n, p,
+                                                    br.ctypes.data, C.byref(prm), C.byref(out), stream))
+    else:
         fn = L.lad_locus_solve_host_f32 if f32 else L.lad_locus_solve_host_f64
-        _check(fn(X.ctypes.data, y.ctypes.data, lam.ctypes.data, None if data_index is None else data_index.ctypes.data,
-                  Bd, B, n, p, C.byref(prm), C.byref(out), stream))
-        res = BatchedSolveResult(beta, obj, it, ev, cv.astype(bool), stt, dsc, stp, solver_id,
-                                 time.perf_counter() - t0)
-    if strict:
-        res.raise_for_status()
-    return res
+        _check(fn(X.ctypes.data, y.ctypes.data, lam.ctypes.data, di, Bd, B, n, p, C.byref(prm), C.byref(out), stream))
+    return BatchedSolveResult(beta, obj, it, ev, cv.astype(bool), stt, dsc, stp, solver_id, time.perf_counter() - t0)
 
 
 def ccd_descend_batched(X, y, lam, start, cfg: CcdConfig | None = None, frozen=None, *,

@@ -84,3 +84,29 @@ def test_oracle_objective_matches_reference(oracle):
         X, Y, b, lam = g[f"x_{m}_{d}"], g[f"y_{m}_{d}"], g[f"beta_{m}_{d}"], g[f"lam_{m}_{d}"]
         got = np.array([oracle.objective(X[i], Y[i], max(float(lam[i]), 1e-9), b[i]) for i in range(len(lam))])
         assert np.array_equal(got, g[f"objective_{m}_{d}"]), (m, d)
+
+
+@pytest.mark.parametrize("variant", ["ternary", "quadrature"])
+def test_oracle_warm_path_matches_reference(oracle, variant):
+    """The warm-started lambda path (paper_2510_15649_b200/path.py's rule, every stage a reference
+    solve_locus with initial_bracket) replayed on the oracle == the reference (warm_path.npz)."""
+    g = load_golden("warm_path")
+    X = np.concatenate([oracle.generate(2, 1, int(g["seed"]), int(f))[0] for f in g["dataset_index"]])
+    assert np.array_equal(X, g["x"])
+    r = oracle.solve_warm_path(g["x"], g["y"], g["lambdas"], outer_search=variant, nthreads=4)
+    assert np.array_equal(r["beta"], g[f"{variant}_beta"])
+    assert np.array_equal(r["objective"], g[f"{variant}_objective"])
+    assert np.array_equal(r["iterations"], g[f"{variant}_iterations"])
+    assert np.array_equal(r["objective_evals"], g[f"{variant}_objective_evals"])
+    assert np.array_equal(r["converged"], g[f"{variant}_converged"])
+
+
+def test_oracle_per_problem_brackets_equal_single_solves(oracle):
+    g = load_golden("bench_cfg0")
+    X, Y, L = g["x"][:6], g["y"][:6], g["lam"][:6]
+    bk = np.array([[-3.0, 3.0], [-1.0, 2.0], [-0.5, 0.5], [2.0, 2.0], [-np.inf, 1.0], [-10.0, 10.0]])
+    r = oracle.solve_locus_batch(X, Y, L, brackets=bk, nthreads=2)
+    assert list(r["status"]) == [0, 0, 0, 2, 2, 0]
+    for i in (0, 1, 2, 5):
+        s = oracle.solve_locus(X[i], Y[i], 1.0, initial_bracket=tuple(bk[i]))
+        assert s.objective == r["objective"][i] and np.array_equal(s.beta, r["beta"][i])
