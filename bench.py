@@ -29,6 +29,7 @@ import subprocess
 import sys
 import tempfile
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -209,6 +210,9 @@ def workload_config(config, a, world):
            "inputs": f"seeded synthetic (Philox keyed by seed {SEEDS[config]} and problem index)"}
     if a.warm:
         cfg["warm"] = True
+        cfg["description"] += ("; warm-started path: largest lambda first, then initial_bracket (-R, R), "
+                               "R = max(1, 2 max|beta_prev|) (paper_2510_15649_b200/path.py), 16 dependent "
+                               "launches per variant")
     return cfg
 
 
@@ -250,7 +254,10 @@ def run_reference(a, rank, world):
             X, Y, L = X.astype(np.float32), Y.astype(np.float32), L.astype(np.float32)
         t0 = time.perf_counter()
         for v in variants:
-            O.solve_locus_batch(X, Y, L, nthreads=nth, outer_search=v)
+            if a.warm:  # the warm lambda path (paper_2510_15649_b200/path.py's rule) on the oracle
+                O.solve_warm_path(X[::16], Y[::16], LAMBDA_GRID, outer_search=v, nthreads=nth)
+            else:
+                O.solve_locus_batch(X, Y, L, nthreads=nth, outer_search=v)
         dt = time.perf_counter() - t0
         if s >= a.warmup:
             times.append(dt)
@@ -534,8 +541,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def flat(path):
+        """(datasets, lambdas, ...) path results as one flat per-solve record per variant"""
+        return SimpleNamespace(**{k: v.reshape((-1,) + tuple(v.shape[2:])) for k, v in path.items()})
+
     def solve(s):
         X, Y, L = wl.inputs(s)
+        if a.warm:  # 16 dependent launches per variant (path.py: largest lambda first, bracketed)
+            return [flat(lad.solve_lambda_path_batched(X, Y, LAMBDA_GRID, c, warm=True)) for c in cfgs]
         return [lad.solve_locus_batched(X, Y, L, c, data_index=wl.data_index) for c in cfgs]
 
     for s in range(a.warmup):
@@ -591,13 +604,19 @@ def main():
         hidx_np = hidx.numpy()
     # untimed warm-up of the host-buffer path at full size (the device memory pool grows to the
     # step's buffers once; the device-side arm likewise runs its warm-up steps untimed)
-    lad.solve_locus_batched(host[0][0], host[0][1], host[0][2], cfgs[0], data_index=hidx_np)
+    if a.warm:
+        lad.solve_lambda_path_batched(host[0][0], host[0][1], LAMBDA_GRID, cfgs[0], warm=True)
+    else:
+        lad.solve_locus_batched(host[0][0], host[0][1], host[0][2], cfgs[0], data_index=hidx_np)
     barrier()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
         h = host[k % n_host]
         for c in cfgs:  # each variant is one public-API call with its own H2D and D2H
-            lad.solve_locus_batched(h[0], h[1], h[2], c, data_index=hidx_np)
+            if a.warm:  # one host-buffer call per lambda stage (inputs and results cross each time)
+                lad.solve_lambda_path_batched(h[0], h[1], LAMBDA_GRID, c, warm=True)
+            else:
+                lad.solve_locus_batched(h[0], h[1], h[2], c, data_index=hidx_np)
     barrier()
     e2e_elapsed = time.perf_counter() - t0
     te = torch.tensor([e2e_elapsed], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
@@ -606,6 +625,9 @@ def main():
     e2e_value = world * e2e_steps * solves_per_step / float(te.item())
     h2d = len(cfgs) * (sum(x.nbytes for x in host[0]) + (hidx_np.nbytes if hidx_np is not None else 0))
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
+    if a.warm:  # per variant: 16 stages x (X, Y, lambda and bracket per dataset)
+        nd = host[0][0].shape[0]
+        h2d = len(cfgs) * 16 * (host[0][0].nbytes + host[0][1].nbytes + nd * 8 + nd * 16)
 
     # DRAM traffic per launch and warp instructions per coordinate step from the committed
     # ncu --set full capture of this workload (None otherwise)
@@ -643,7 +665,13 @@ def main():
             X64, Y64, L64 = Xh.astype(np.float64), Yh.astype(np.float64), np.asarray(Lh, dtype=np.float64)
             Xh, Yh, Lh = Xh.astype(np.float32), Yh.astype(np.float32), np.asarray(Lh, dtype=np.float32)
         t0 = time.perf_counter()
-        ros = [O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=v) for v in wl.variants]
+        if a.warm:  # the oracle replay of the warm path on the sample's datasets (same rule, path.py)
+            nd = Xh.shape[0] // 16
+            ros = [{k: v.reshape((-1,) + v.shape[2:]) for k, v in
+                    O.solve_warm_path(Xh[::16], Yh[::16], LAMBDA_GRID, outer_search=v, nthreads=nth).items()}
+                   for v in wl.variants]
+        else:
+            ros = [O.solve_locus_batch(Xh, Yh, Lh, nthreads=nth, outer_search=v) for v in wl.variants]
         dt = time.perf_counter() - t0
         nsol = Xh.shape[0]
         cpu = {"value": nsol * len(ros) / dt, "unit": "solves/s", "cores": nth, "kind": "port",
