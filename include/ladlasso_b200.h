@@ -191,12 +191,26 @@ int lad_lp_solve_f64(const double *X, const double *Y, const double *lam, int64_
 int lad_objective_f64(const double *X, const double *Y, const double *lam, int64_t B, int32_t n, int32_t p,
                       const double *beta, double lambda_floor, double *objective, void *stream);
 
+/* Batched datagen.generate(GenSpec) (datagen.py:63-80, rng.py:25-72) on the device: B
+ * problems of one shape (m, d), problem i seeded with seeds[i] (the other GenSpec fields
+ * shared).  true_coefficients (d,) or NULL (U[1,10] on the first n_informative axes).
+ * Outputs X (B, m, d), Y (B, m), beta_true (B, d) or NULL; device pointers.  The
+ * transcendentals are double-double and rounded once (see lad_genspec.cuh); equality with
+ * the host generator is measured in tests/test_gpu_genspec.py (tolerance 1 ulp).
+ * d <= 8, m <= 1024 (LAD_E_UNSUPPORTED beyond). */
+int lad_genspec_generate_f64(int64_t B, int32_t m, int32_t d, int32_t n_informative,
+                             const double *true_coefficients, double noise_sigma, double outlier_fraction,
+                             double outlier_scale, const uint64_t *seeds, double *X, double *Y, double *beta_true,
+                             void *stream);
+
 /* Device-side problem generation for the BASELINE.json configs:
  *   config 0/2: X~N(0,1), 2 nonzeros +-U[1,3], Laplace(0,0.5), 10% rows +-10
  *   config 1:   X~U(-1,1), beta~N(0,1), Laplace(0,0.3), lambda~U(0.1,2)
  *   config 4:   X~t(3), 3 nonzeros +-U[1,3], Cauchy(0,0.2)
  * Problem i uses counter-based Philox keyed by (seed, first + i), so any shard
- * [first, first+B) is reproducible independently.  lam may be NULL except for config 1. */
+ * [first, first+B) is reproducible independently.  lam may be NULL except for config 1.
+ * Every operation is a single IEEE operation with this library's own transcendental
+ * polynomials (lad_gen.cuh), so oracle/gen_host.c reproduces the bytes on the CPU. */
 int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, int64_t B, int32_t n, int32_t p, double *X,
                      double *Y, double *lam, double *beta_true, void *stream);
 

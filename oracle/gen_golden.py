@@ -467,6 +467,46 @@ def gen_warm(pool):
     print("warm_path.npz", flush=True)
 
 
+def gen_genspec(pool):
+    """datagen.generate (datagen.py:63-80) on specs beyond the acceptance grid: up to 1000 rows,
+    d = 8, informative subsets, fixed true coefficients, sigma 0, odd draw counts (the Box-Muller
+    spare crossing phases), large seeds."""
+    _ref()
+    from ladlasso.datagen import GenSpec, generate
+
+    rng = np.random.default_rng(2510)
+    specs = []
+    for k in range(40):
+        m = int(rng.choice([1, 3, 7, 30, 31, 64, 129, 300, 1000]))
+        d = int(rng.integers(1, 9))
+        has_truth = k % 5 == 3
+        truth = tuple(float(v) for v in rng.standard_normal(d)) if has_truth else None
+        specs.append(dict(m=m, d=d, n_informative=int(rng.integers(1, d + 1)), true_coefficients=truth,
+                          noise_sigma=float(rng.choice([0.0, 0.5, 1.0, 3.0])),
+                          outlier_fraction=float(rng.choice([0.0, 0.1, 0.25, 0.5])),
+                          outlier_scale=float(rng.choice([1.0, 10.0, 50.0])),
+                          seed=int(rng.integers(0, 2 ** 63)) if k % 3 else k))
+    Mx, Dx = 1000, 8
+    B = len(specs)
+    out = dict(x=np.full((B, Mx, Dx), np.nan), y=np.full((B, Mx), np.nan), beta=np.full((B, Dx), np.nan),
+               truth=np.zeros((B, Dx)), has_truth=np.zeros(B, bool))
+    for key in ("m", "d", "n_informative", "seed"):
+        out[key] = np.array([s[key] for s in specs], dtype=np.uint64 if key == "seed" else np.int64)
+    for key, src in (("sigma", "noise_sigma"), ("fraction", "outlier_fraction"), ("scale", "outlier_scale")):
+        out[key] = np.array([s[src] for s in specs])
+    for k, sp in enumerate(specs):
+        data, beta = generate(GenSpec(**sp))
+        m, d = sp["m"], sp["d"]
+        out["x"][k, :m, :d] = data.x
+        out["y"][k, :m] = data.y
+        out["beta"][k, :d] = beta.beta
+        if sp["true_coefficients"] is not None:
+            out["truth"][k, :d] = sp["true_coefficients"]
+            out["has_truth"][k] = True
+    np.savez_compressed(os.path.join(GOLDEN, "genspec.npz"), **out)
+    print("genspec.npz", flush=True)
+
+
 def _objective_task(args):
     _ref()
     from ladlasso.model import Coefficients, Dataset, ProblemSpec, evaluate_objective
@@ -753,7 +793,7 @@ def main():
                          ("params", gen_params), ("configs", lambda p: gen_configs(p, a.quick)),
                          ("cli", gen_cli), ("curve", gen_curve), ("lp", gen_lp), ("large", gen_large),
                          ("bench", lambda p: gen_bench(p, a.quick)), ("objective", gen_objective),
-                         ("warm", gen_warm)):
+                         ("warm", gen_warm), ("genspec", gen_genspec)):
             if only is None or name in only:
                 fn(pool)
 

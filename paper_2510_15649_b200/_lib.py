@@ -35,6 +35,7 @@ SYMBOLS = (
     "lad_lp_solve_f64",
     "lad_locus_solve_bracketed_f64",
     "lad_locus_solve_bracketed_host_f64",
+    "lad_genspec_generate_f64",
 )
 
 LAD_OK = 0
@@ -126,6 +127,7 @@ def load(build_if_missing: bool = False):
     L.lad_locus_solve_bracketed_f64.argtypes = [vp, vp, vp, vp, i64, i64, i32, i32, vp, C.POINTER(LocusParams),
                                                 C.POINTER(LocusOut), vp]
     L.lad_locus_solve_bracketed_host_f64.argtypes = L.lad_locus_solve_bracketed_f64.argtypes
+    L.lad_genspec_generate_f64.argtypes = [i64, i32, i32, i32, vp, dbl, dbl, dbl, vp, vp, vp, vp, vp]
     L.lad_fp64_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
     L.lad_fp32_peak_tflops.argtypes = [C.POINTER(C.c_double), vp]
     L.lad_locus_solve_f32.argtypes = L.lad_locus_solve_f64.argtypes

@@ -19,6 +19,7 @@
 #include "lad_cert.cuh"
 #include "lad_lp.cuh"
 #include "lad_gen.cuh"
+#include "lad_genspec.cuh"
 #include "lad_locus.cuh"
 #include "lad_locus_warp.cuh"
 #include "lad_locus_block.cuh"
@@ -631,6 +632,39 @@ extern "C" int lad_generate_f64(int32_t config, uint64_t seed, int64_t first, in
     if (B == 0) return LAD_OK;
     lad::GenArgs G{config, seed, first, B, n, p, X, Y, lam, beta_true};
     lad::gen_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(G); ++g_launches;
+    CK(cudaGetLastError());
+    return LAD_OK;
+}
+
+extern "C" int lad_genspec_generate_f64(int64_t B, int32_t m, int32_t d, int32_t n_informative,
+                                        const double *true_coefficients, double noise_sigma, double outlier_fraction,
+                                        double outlier_scale, const uint64_t *seeds, double *X, double *Y,
+                                        double *beta_true, void *stream)
+{
+    // GenSpec.__post_init__ (datagen.py:40-58)
+    if (m < 1 || d < 1) return fail(LAD_E_INVALID, "need m >= 1 and d >= 1");
+    if (n_informative < 1 || n_informative > d)
+        return fail(LAD_E_INVALID, "n_informative must be in [1, %d], got %d", d, n_informative);
+    if (!(noise_sigma >= 0)) return fail(LAD_E_INVALID, "noise_sigma must be >= 0");
+    if (!(outlier_fraction >= 0 && outlier_fraction < 1)) return fail(LAD_E_INVALID, "outlier_fraction must be in [0, 1)");
+    if (!(outlier_scale >= 1)) return fail(LAD_E_INVALID, "outlier_scale must be >= 1");
+    if (d > 8 || m > 1024) return fail(LAD_E_UNSUPPORTED, "device GenSpec generation supports d <= 8, m <= 1024");
+    if (B < 0 || (B > 0 && (!seeds || !X || !Y))) return fail(LAD_E_INVALID, "bad batch arguments");
+    if (B == 0) return LAD_OK;
+    lad::GenSpecArgs G;
+    G.B = B;
+    G.m = m;
+    G.d = d;
+    G.n_informative = n_informative;
+    G.n_outliers = (int)std::floor(outlier_fraction * (double)m);  // math.floor(fraction * m)
+    G.truth = true_coefficients;
+    G.noise_sigma = noise_sigma;
+    G.outlier_scale = outlier_scale;
+    G.seeds = seeds;
+    G.X = X;
+    G.Y = Y;
+    G.beta_true = beta_true;
+    lad::genspec_kernel<<<(unsigned)((B + 63) / 64), 64, 0, (cudaStream_t)stream>>>(G); ++g_launches;
     CK(cudaGetLastError());
     return LAD_OK;
 }

@@ -28,7 +28,7 @@ import numpy as np
 from .errors import InvalidInputError
 from .solver import Coefficients, Dataset
 
-__all__ = ["Pcg32", "GenSpec", "generate", "write_dataset_csv", "read_dataset_csv", "metadata_path",
+__all__ = ["Pcg32", "GenSpec", "generate", "generate_batched", "write_dataset_csv", "read_dataset_csv", "metadata_path",
            "write_metadata", "read_metadata"]
 
 _M64 = 0xFFFFFFFFFFFFFFFF
@@ -149,6 +149,41 @@ def generate(g: GenSpec) -> tuple[Dataset, Coefficients]:
     noise[rows] *= g.outlier_scale
     response = design @ truth + noise
     return Dataset(design, response), Coefficients(truth)
+
+
+def generate_batched(specs, device="cuda"):
+    """``generate`` for many GenSpecs at once ON THE DEVICE (lad_genspec_generate_f64, one
+    thread per problem): returns CUDA tensors X (B, m, d), y (B, m), beta_true (B, d).  The
+    specs may differ only in their seeds.  The transcendentals are double-double and rounded
+    once, so the result equals ``generate`` wherever glibc's log/sin/cos are correctly rounded
+    (all golden inputs; tests/test_gpu_genspec.py bounds any difference by 1 ulp)."""
+    import torch
+
+    from . import _lib
+    from .solver import _check
+
+    specs = list(specs)
+    if not specs:
+        raise InvalidInputError("need at least one GenSpec")
+    g0 = specs[0]
+    key = lambda g: (g.m, g.d, g.n_informative, g.true_coefficients, g.noise_sigma, g.outlier_fraction,
+                     g.outlier_scale)
+    if any(key(g) != key(g0) for g in specs[1:]):
+        raise InvalidInputError("generate_batched: specs must differ only in their seeds")
+    dev = torch.device(device)
+    B, m, d = len(specs), g0.m, g0.d
+    seeds = torch.from_numpy(np.array([g.seed & _M64 for g in specs], dtype=np.uint64).view(np.int64)).to(dev)
+    X = torch.empty((B, m, d), dtype=torch.float64, device=dev)
+    y = torch.empty((B, m), dtype=torch.float64, device=dev)
+    bt = torch.empty((B, d), dtype=torch.float64, device=dev)
+    truth = None
+    if g0.true_coefficients is not None:
+        truth = torch.tensor(g0.true_coefficients, dtype=torch.float64, device=dev)
+    _check(_lib.load().lad_genspec_generate_f64(
+        B, m, d, g0.n_informative, truth.data_ptr() if truth is not None else None, float(g0.noise_sigma),
+        float(g0.outlier_fraction), float(g0.outlier_scale), seeds.data_ptr(), X.data_ptr(), y.data_ptr(),
+        bt.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    return X, y, bt
 
 
 def _csv_header(d: int) -> str:
