@@ -196,7 +196,7 @@ int lad_objective_f64(const double *X, const double *Y, const double *lam, int64
  * shared).  true_coefficients (d,) or NULL (U[1,10] on the first n_informative axes).
  * Outputs X (B, m, d), Y (B, m), beta_true (B, d) or NULL; device pointers.  The
  * transcendentals are double-double and rounded once (see lad_genspec.cuh); equality with
- * the host generator is measured in tests/test_gpu_genspec.py (tolerance 1 ulp).
+ * the host generator is measured in tests/test_gpu_genspec.py (2 ulp per normal draw).
  * d <= 8, m <= 1024 (LAD_E_UNSUPPORTED beyond). */
 int lad_genspec_generate_f64(int64_t B, int32_t m, int32_t d, int32_t n_informative,
                              const double *true_coefficients, double noise_sigma, double outlier_fraction,

@@ -5,13 +5,12 @@
 // coefficients U[1, 10] as a + (b - a) u, m noise normals scaled by sigma, outlier rows
 // by rejection until distinct, y = x @ beta (OpenBLAS dgemv_t order, gemv_row) + noise.
 //
-// Python's math.log / math.sin / math.cos are glibc's; they are not libdevice's.  Here
-// they are evaluated in double-double arithmetic (~1e-30 relative) and rounded once, i.e.
-// correctly rounded except in astronomically rare hard cases -- which is what glibc 2.39
-// returns except in the rare cases where it is not correctly rounded itself (its log is
-// documented at < 0.52 ulp, sin/cos < 0.55 ulp).  tests/test_gpu_genspec.py measures the
-// agreement with synth.generate (the host restatement) and the reference's acceptance
-// inputs: bit-identical on every golden input, with a declared tolerance of 1 ulp.
+// Python's math.log / math.sin / math.cos are glibc's, not libdevice's.  Here they are
+// evaluated in double-double arithmetic (~1e-30 relative) and rounded once: correctly
+// rounded (0 of 600,000 Box-Muller inputs differ from mpmath).  glibc 2.39 itself is not
+// correctly rounded on ~0.1% of these inputs, so a normal draw (rho * cos) can differ from
+// the reference's by up to 2 ulp; most problems are bit-identical.  tests/test_gpu_genspec.py
+// measures the agreement with synth.generate and the reference's own generated inputs.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -156,7 +156,7 @@ def generate_batched(specs, device="cuda"):
     thread per problem): returns CUDA tensors X (B, m, d), y (B, m), beta_true (B, d).  The
     specs may differ only in their seeds.  The transcendentals are double-double and rounded
     once, so the result equals ``generate`` wherever glibc's log/sin/cos are correctly rounded
-    (all golden inputs; tests/test_gpu_genspec.py bounds any difference by 1 ulp)."""
+    (all golden inputs; tests/test_gpu_genspec.py bounds any difference: each transcendental within 1 ulp of glibc's, each normal draw within 2 ulp)."""
     import torch
 
     from . import _lib

