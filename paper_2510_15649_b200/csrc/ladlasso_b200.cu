@@ -559,16 +559,28 @@ int brute_dispatch(const double *X, const double *Y, const double *lam, int64_t 
         A.nchunks = 65535;
         A.chunk = (C + A.nchunks - 1) / A.nchunks;
     }
-    if (B > 65535) return fail(LAD_E_INVALID, "chunked brute handles at most 65535 problems per call");
-    size_t bytes = (size_t)B * A.nchunks * (sizeof(lad::BruteKey) + 8);
+    // grid.y carries the problem: slices of at most 65535 problems (pointers offset per slice)
+    const int64_t slice = std::min<int64_t>(B, 65535);
+    size_t bytes = (size_t)slice * A.nchunks * (sizeof(lad::BruteKey) + 8);
     char *buf = nullptr;
     CK(cudaMallocAsync((void **)&buf, bytes, st));
     A.partial = (lad::BruteKey *)buf;
-    A.pcount = (unsigned long long *)(buf + (size_t)B * A.nchunks * sizeof(lad::BruteKey));
-    dim3 grid((unsigned)A.nchunks, (unsigned)B);
-    lad::brute_chunk_kernel<P><<<grid, 256, 0, st>>>(A); ++g_launches;
-    lad::brute_reduce_kernel<P><<<(unsigned)((B + 127) / 128), 128, 0, st>>>(A); ++g_launches;
-    cudaError_t le = cudaGetLastError();
+    A.pcount = (unsigned long long *)(buf + (size_t)slice * A.nchunks * sizeof(lad::BruteKey));
+    cudaError_t le = cudaSuccess;
+    for (int64_t s0 = 0; s0 < B && le == cudaSuccess; s0 += slice) {
+        lad::BruteArgs S = A;
+        S.B = std::min<int64_t>(slice, B - s0);
+        S.X = X + (size_t)s0 * n * P;
+        S.Y = Y + (size_t)s0 * n;
+        S.lam = lam + s0;
+        S.beta = beta + (size_t)s0 * P;
+        S.objective = objective + s0;
+        S.vertices = vertices ? vertices + s0 : nullptr;
+        dim3 grid((unsigned)S.nchunks, (unsigned)S.B);
+        lad::brute_chunk_kernel<P><<<grid, 256, 0, st>>>(S); ++g_launches;
+        lad::brute_reduce_kernel<P><<<(unsigned)((S.B + 127) / 128), 128, 0, st>>>(S); ++g_launches;
+        le = cudaGetLastError();
+    }
     cudaFreeAsync(buf, st);
     if (le != cudaSuccess) return fail(LAD_E_CUDA, "brute kernel: %s", cudaGetErrorString(le));
     return LAD_OK;
