@@ -138,3 +138,17 @@ def test_big_endian_host_arrays():
     be = [a.astype(a.dtype.newbyteorder(">")) for a in (X, Y, L)]
     assert np.array_equal(lad.solve_brute_batched(*be)[1], ref)
     assert np.array_equal(lad.solve_locus_batched(*be).objective, lad.solve_locus_batched(X, Y, L).objective)
+
+
+def test_brute_chunked_path_beyond_65535_problems(oracle):
+    """C(33,3) = 5456 > 4096 vertices takes the block-per-(problem, chunk) path, whose grid.y holds
+    at most 65535 problems: larger batches run in slices."""
+    B = 65535 + 77
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((B, 30, 3))
+    Y = rng.standard_normal((B, 30))
+    L = rng.uniform(0.1, 2.0, B)
+    bb, bo, bv = lad.solve_brute_batched(X, Y, L)
+    for i in (0, 65534, 65535, 65536, B - 1):
+        ob, oo, on = oracle.solve_brute(X[i], Y[i], float(L[i]))
+        assert float(bo[i]) == oo and np.array_equal(np.asarray(bb[i]), ob) and int(bv[i]) == on, i
