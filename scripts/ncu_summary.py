@@ -1,6 +1,6 @@
 """Summarise ncu --set full captures of the library's kernels into profiles/ncu_traffic.json.
 
-usage: python scripts/ncu_summary.py OUTDIR WORKLOAD...   (reads OUTDIR/prof_WORKLOAD.ncu-rep and
+usage: python scripts/ncu_summary.py [--db OUT.json] OUTDIR WORKLOAD...   (reads OUTDIR/prof_WORKLOAD.ncu-rep and
 OUTDIR/units_WORKLOAD.json written by scripts/gpurun/r2_profile_all.sh)
 Per workload: kernel duration, warp instructions per work unit (coordinate step / vertex / pivot /
 problem), issue-slot utilisation, resident warps, active threads per warp, FP64 / LSU / ALU pipe
@@ -75,8 +75,13 @@ def summarise(rep, units):
 
 
 def main():
-    out, works = sys.argv[1], sys.argv[2:]
+    args = sys.argv[1:]
     path = os.path.join("profiles", "ncu_traffic.json")
+    if "--db" in args:  # write elsewhere (on the GPU box: under gpurun_out/, merged here afterwards)
+        i = args.index("--db")
+        path = args[i + 1]
+        del args[i:i + 2]
+    out, works = args[0], args[1:]
     db = json.load(open(path)) if os.path.exists(path) else {}
     for w in works:
         rep = os.path.join(out, f"prof_{w}.ncu-rep")
