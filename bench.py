@@ -362,6 +362,34 @@ def brute_flops(vertices, m, d):
     return vertices * (2.0 / 3.0 * d ** 3 + 2 * d * d + 2 * m * d + 2 * m + 2 * d)
 
 
+def ncu_lookup(key, solves_per_launch, units, elapsed, clocks, dev, unit):
+    """`traffic` (DRAM bytes per launch) and `issue_roofline` of a bench line from the committed ncu
+    --set full summary profiles/ncu_traffic.json[key]: bytes per solve x solves per launch, and warp
+    instructions per work unit x the live work-unit rate against 4 warp instructions per SM per cycle
+    at the sampled SM clock.  (None, None) without a capture of this workload."""
+    import torch
+
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(key)
+    except (OSError, ValueError):
+        return None, None
+    if not tr:
+        return None, None
+    traffic = tr["bytes_per_solve"] * solves_per_launch if tr.get("bytes_per_solve") is not None else None
+    issue = None
+    ipu = tr.get("warp_instr_per_coord_step") if unit == "coordinate step" else tr.get("warp_instr_per_unit")
+    if ipu and clocks.get("sm_mhz") and elapsed > 0:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_issue = 4 * sms * clocks["sm_mhz"] * 1e6  # one warp instruction per SMSP per cycle
+        ach = ipu * units / elapsed
+        issue = {"bound": "issue", "achieved": ach / 1e9, "peak": peak_issue / 1e9, "unit": "G warp-instr/s",
+                 "frac": ach / peak_issue, f"warp_instr_per_{unit.replace(' ', '_')}": ipu,
+                 "ncu_issue_active_pct": tr.get("issue_active_pct"), "ncu_key": key,
+                 "source": f"instr/{unit} from profiles/ncu_traffic.json x live {unit}s/s; "
+                           "peak = 4 SMSPs x SMs x sampled SM clock"}
+    return traffic, issue
+
+
 def run_aux(a, world, rank, local):
     """--solver lp | brute: the widened rows (the check of §8a a17), same protocol."""
     import torch
@@ -439,21 +467,28 @@ def run_aux(a, world, rank, local):
     value = world * a.steps * B / float(t.item())
     fl = sum(flops(r) for r in results)
     achieved = fl / elapsed / 1e12
-    # e2e through the public API with host (pinned) inputs and host outputs
+    # work units of the timed launches (pivots / nonsingular vertices) for the issue roofline
+    units = sum(float(r.pivots.double().sum()) if a.solver == "lp" else float(r[2].double().sum()) for r in results)
+    # e2e through the public API with host (pinned) inputs and host outputs, over the same number of
+    # steps as the device-timed region (distinct host inputs within 2 GiB of pinned memory, cycled)
+    step_bytes = sum(v.numel() * v.element_size() for v in steps_inputs[a.warmup])
+    n_host = max(1, min(a.steps, (2 << 30) // max(1, step_bytes)))
     hosts = []
-    for k in range(min(a.steps, 3)):
+    for k in range(n_host):
         hx, hy, hl = (torch.empty(v.shape, dtype=v.dtype, pin_memory=True).copy_(v) for v in steps_inputs[a.warmup + k])
         hosts.append((hx.numpy(), hy.numpy(), hl.numpy()))
     run_host = (lambda h: lad.solve_lp_batched(*h)) if a.solver == "lp" else (lambda h: lad.solve_brute_batched(*h))
     run_host(hosts[0])  # untimed full-size warm-up (allocator and pool growth)
     barrier()
     t0 = time.perf_counter()
-    for h in hosts:
-        run_host(h)
+    for k in range(a.steps):
+        run_host(hosts[k % n_host])
     barrier()
-    e2e_value = world * len(hosts) * B / (time.perf_counter() - t0)
+    e2e_value = world * a.steps * B / (time.perf_counter() - t0)
     h2d = sum(v.nbytes for v in hosts[0])
     d2h = B * (p * 8 + 8 + 4 + 1 + 1) if a.solver == "lp" else B * (p * 8 + 8 + 8)
+    traffic, issue = ncu_lookup(f"{a.solver}_f64", B, units, elapsed, clocks, dev,
+                                "pivot" if a.solver == "lp" else "nonsingular vertex")
     cpu = parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
         from oracle import oracle as O
@@ -492,11 +527,13 @@ def run_aux(a, world, rank, local):
                        "solves_per_step_per_gpu": B, "parallelism": f"shard{world} (independent problems)",
                        "l2": "flushed between steps (256 MiB memset)"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per solve) x solves per launch",
                          "flops_model": "bench.lp_flops" if a.solver == "lp" else "bench.brute_flops"},
+            "issue_roofline": issue,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "steps": len(hosts)},
+                    "d2h_bytes_per_step": int(d2h), "steps": a.steps, "distinct_input_steps": n_host},
             "gpu_launches": gpu_launches, "clocks": clocks, "parity_sample": parity, "step_ms": step_ms}),
             flush=True)
     if world > 1:
@@ -631,25 +668,8 @@ def main():
 
     # DRAM traffic per launch and warp instructions per coordinate step from the committed
     # ncu --set full capture of this workload (None otherwise)
-    traffic = None
-    issue = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"config{a.config}_{a.dtype}")
-        if tr:
-            if tr.get("bytes_per_solve") is not None:
-                traffic = tr["bytes_per_solve"] * wl.solves  # per launch (one call per variant and step)
-            ipc = tr.get("warp_instr_per_coord_step")
-            if ipc and clocks.get("sm_mhz"):
-                sms = torch.cuda.get_device_properties(dev).multi_processor_count
-                peak_issue = 4 * sms * clocks["sm_mhz"] * 1e6  # one warp instruction per SMSP per cycle
-                ach_issue = ipc * S / elapsed
-                issue = {"bound": "issue", "achieved": ach_issue / 1e9, "peak": peak_issue / 1e9,
-                         "unit": "G warp-instr/s", "frac": ach_issue / peak_issue,
-                         "warp_instr_per_coord_step": ipc,
-                         "source": "instr/step from profiles/ncu_traffic.json x live coordinate steps/s; "
-                                   "peak = 4 SMSPs x SMs x sampled SM clock"}
-    except (OSError, ValueError, KeyError, TypeError):
-        pass
+    key = f"config{a.config}{'_warm' if a.warm else ''}_{a.dtype}"
+    traffic, issue = ncu_lookup(key, wl.solves, S, elapsed, clocks, dev, "coordinate step")
     cpu = None
     parity = None
     fp32_dist = None

@@ -159,6 +159,7 @@ struct Ctl {
     // counters
     int D;
     long long S;
+    const double *ysrc;  // thread kernel with y read from global memory: the problem's y row
 };
 
 // ---------------------------------------------------------------------------
@@ -182,13 +183,13 @@ __device__ double col_abs_sum(const double *Xs, int n, int p, int j, int lane)
 }
 
 template <int NMAX, int PMAX>
-__device__ double objective_of(const double *Xs, const double *Ys, int n, int p, int lane, double lam,
+__device__ double objective_of(const double *Xs, const double *Yp, int ys, int n, int p, int lane, double lam,
                                const double *b)
 {
     double rs = np_sum(n, [&](int i) {
         double g = gemv_row(p, i, n, [&](int jj) { return xs_at<NMAX, PMAX>(Xs, i, jj, lane); },
                             [&](int jj) { return b[jj]; });
-        return fabs(dsub(Ys[i * 32 + lane], g));
+        return fabs(dsub(Yp[i * ys], g));
     });
     double bs = np_sum(p, [&](int jj) { return fabs(b[jj]); });
     return dadd(rs, dmul(lam, bs));
@@ -322,6 +323,8 @@ template <int NMAX, int PMAX>
 struct ThreadAccess {
     int n, p, lane;
     double *Xs, *Ys;
+    double *Tw;  // per axis: sum of the breakpoint weights (|x_ij| and lambda), any order (median guess test)
+    double *RX;  // RN(1 / x_ij), same layout as Xs (division by reciprocal), or null
     __device__ __forceinline__ bool leader() const { return true; }
     __device__ __forceinline__ void sync() const {}
     // count one finished unit on *ctr; true for the caller that completes `of` units
@@ -354,18 +357,29 @@ struct ThreadAccess {
         for (int i = 0; i < n; ++i) {
             double yv = yg[i];
             ok = ok && isfinite(yv);
-            Ys[i * 32 + lane] = yv;
+            if (Ys != nullptr) Ys[i * 32 + lane] = yv;
             for (int j = 0; j < p; ++j) {
                 double xv = xg[i * p + j];
                 ok = ok && isfinite(xv);
                 if (xv == 0.0) mask |= 1u << j;
                 Xs[(i * PMAX + j) * 32 + lane] = xv;
+                if (RX != nullptr) {
+                    RX[(i * PMAX + j) * 32 + lane] = rcp_rn(xv);
+                    if (!div_operand_safe(xv)) mask |= 1u << j;  // the column takes the generic path (IEEE division)
+                }
             }
         }
         double lraw = A.lam[pr];
         ok = ok && isfinite(lraw) && lraw >= 0.0;
         C.lam = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
         C.sparse_mask = mask;
+        C.ysrc = yg;
+        if (Tw != nullptr)
+            for (int j = 0; j < p; ++j) {
+                double s = C.lam;
+                for (int i = 0; i < n; ++i) s += fabs(Xs[(i * PMAX + j) * 32 + lane]);
+                Tw[j * 32 + lane] = s;
+            }
         if (!ok) {
             write_invalid<PMAX>(A, (int64_t)pr, p);
             return 0;
@@ -373,11 +387,11 @@ struct ThreadAccess {
         return 1;
     }
     __device__ double col_abs_sum(int j) const { return lad::col_abs_sum<NMAX, PMAX>(Xs, n, p, j, lane); }
-    __device__ double y_absmax() const
+    __device__ double y_absmax(const double *ysrc) const
     {
         double ymax = 0.0;
         for (int i = 0; i < n; ++i) {
-            double a = fabs(Ys[i * 32 + lane]);
+            double a = fabs(Ys != nullptr ? Ys[i * 32 + lane] : __ldg(ysrc + i));
             if (i == 0 || a > ymax) ymax = a;
         }
         return ymax;
@@ -395,7 +409,7 @@ struct ThreadAccess {
 // warp-per-problem kernels (in the latter all 32 lanes run it in lock-step
 // on a shared Ctl, with identical values).
 template <int PMAX, class AC>
-__device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const AC &acc, int slot)
+__device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A, const AC &acc, int slot)
 {
     const int n = acc.n;
     const int p = acc.p;
@@ -453,7 +467,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
                 C.R_lo = A.prm.bracket_lo;
                 C.R_hi = A.prm.bracket_hi;
             } else {
-                double ymax = acc.y_absmax();
+                double ymax = acc.y_absmax(C.ysrc);
                 double radius = scale > 0.0 ? ddiv(ymax, scale) : __longlong_as_double(0x7ff0000000000000LL);
                 if (!isfinite(radius) || radius <= 0.0) radius = 1.0;
                 C.R_lo = -radius;
@@ -922,9 +936,41 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 #undef ISSUE
 #undef PROBE
 
+// Out-of-line controller (the warp kernels: a cold path next to the step loop).
+template <int PMAX, class AC>
+__device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const AC &acc, int slot)
+{
+    return controller_body<PMAX, AC>(C, A, acc, slot);
+}
+
+// Thread kernel: the controller inlined into the main loop (no call ABI: no
+// callee-saved register saves and restores in local memory around every
+// descent).  Config 1, same-box A/B at B = 262,144: 5.93 M -> 6.19 M solves/s
+// at the old 96-register cap, 8.30 M with the cap raised (below).
+#ifndef LAD_THREAD_INLINE_CTL
+#define LAD_THREAD_INLINE_CTL 1
+#endif
+
 // ---------------------------------------------------------------------------
 // hot path: one exact coordinate step (ccd.py:160-193)
 // ---------------------------------------------------------------------------
+
+// Thread kernel's weighted median: guess the axis' previous median first
+// (step_dense_cand) instead of sorting every step (step_dense).
+#ifndef LAD_THREAD_CAND
+#define LAD_THREAD_CAND 0
+#endif
+// Thread kernel's breakpoint division by a per-problem reciprocal table in
+// shared memory (div_by_rcp: Markstein, bit-identical to r / x), columns with
+// a divisor outside 2^+-450 on the generic path.
+#ifndef LAD_THREAD_RCP
+#define LAD_THREAD_RCP 0
+#endif
+// Thread kernel (compile-time shape): y read from global memory (L1) at the
+// per-descent residual and objective instead of a shared-memory copy.
+#ifndef LAD_THREAD_YGLOBAL
+#define LAD_THREAD_YGLOBAL 0
+#endif
 
 // beta register array accessed with a runtime axis index (select chains, no
 // local memory)
@@ -946,18 +992,20 @@ __device__ __forceinline__ void bset(double (&b)[PMAX], int j, double v)
 // Dense column, compile-time n = NMAX: register sort network.
 // Returns true if the step moved beta_j.
 template <int NMAX, int PMAX>
-__device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, double *Ls,
-                                           int lane, int j, double lam, double &f_cur, double &sum_abs_b)
+__device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, const double *RX,
+                                           double *Ls, int lane, int j, double lam, double &f_cur, double &sum_abs_b)
 {
     constexpr int NE = NMAX + 1;
     constexpr int XS = PMAX * 32;  // row stride of Xs in doubles
     const double *xc = Xs + j * 32 + lane;
+    const double *rc = RX + j * 32 + lane;
     const double bj = bget(b, j);
     double key[NE];
     int idx[NE];
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
-        double loc = dadd(ddiv(r[i], xc[i * XS]), bj);  // np.divide then += b[j] (ccd.py:165-166)
+        // np.divide then += b[j] (ccd.py:165-166)
+        double loc = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : ddiv(r[i], xc[i * XS]), bj);
         key[i] = loc;
         idx[i] = i;
         Ls[i * 32 + lane] = loc;
@@ -1005,6 +1053,133 @@ __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX],
     double v_new = dadd(constant, dot);
     if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
         double delta = dsub(t_new, bj);
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+        sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+        bset(b, j, t_new);
+        f_cur = v_new;
+    }
+}
+
+// Dense column, compile-time n = NMAX, with the median guessed first: the
+// element that was this axis' weighted median at its previous step (cand) is
+// usually still the median.  Element m is the reference's median iff the
+// weight ordered before it in the stable (location, index) order, Wb,
+// satisfies Wb < total/2 <= Wb + w_m in numpy's sequential cumsum
+// (ccd.py:83-88).  Wb and the total are summed here in index order, and the
+// guess is accepted only beyond a margin of 1e-9 * total on both sides: every
+// sum of NE <= 33 non-negative terms is within NE * 2^-53 * total of the
+// exact one (ours and numpy's), so an accepted guess is numpy's k, and the
+// 1e-12 * total midpoint tie (ccd.py:89-90) is excluded.  Otherwise the
+// register sort network decides as in step_dense and refreshes the guess.
+// Breakpoints stay in registers in index order for v_new (no reload); the
+// guess' location is read back through the lane's Ls column.
+constexpr double THREAD_MEDIAN_MARGIN = 1e-9;
+
+
+struct MedianPick {
+    double t;
+    int ik;  // index of the element at the median position
+};
+
+// The miss path of step_dense_cand, out of line (it keeps the guess path's
+// registers free): the breakpoints are re-read from the lane's Ls column and
+// ordered by the register sort network, then numpy's cumsum decides
+// (ccd.py:83-90), as in step_dense.
+template <int NMAX, int PMAX>
+__device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double *xc, int lane, double lam)
+{
+    constexpr int NE = NMAX + 1;
+    constexpr int XS = PMAX * 32;
+    double key[NE];
+    int idx[NE];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        key[i] = Ls[i * 32 + lane];
+        idx[i] = i;
+    }
+    sort_pairs<NE>(key, idx);
+    auto wsorted = [&](int id) -> double {
+        int ic = id < NMAX ? id : NMAX - 1;
+        double x = xc[ic * XS];
+        return id < NMAX ? fabs(x) : lam;
+    };
+    double c = 0.0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) c = dadd(c, wsorted(idx[k]));
+    const double tot = c;
+    const double hf = dmul(0.5, tot);
+    c = 0.0;
+    bool found = false;
+    int kk = NE;
+    double ck = 0.0, tk = key[NE - 1], tk1 = key[NE - 1];
+    int ik = idx[NE - 1];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        c = dadd(c, wsorted(idx[k]));
+        bool hit = !found && (c >= hf);
+        if (hit) {
+            kk = k;
+            ck = c;
+            tk = key[k];
+            tk1 = key[k + 1 < NE ? k + 1 : k];
+            ik = idx[k];
+        }
+        found = found || hit;
+    }
+    MedianPick mp;
+    mp.t = (kk + 1 < NE && fabs(dsub(ck, hf)) <= dmul(1e-12, tot)) ? dmul(0.5, dadd(tk, tk1)) : tk;
+    mp.ik = ik;
+    return mp;
+}
+
+template <int NMAX, int PMAX>
+__device__ __forceinline__ void step_dense_cand(double (&r)[NMAX], double (&b)[PMAX], int (&cand)[PMAX],
+                                                const double *Xs, const double *RX, double *Ls, const double *Tw,
+                                                int lane, int j, double lam, double &f_cur, double &sum_abs_b)
+{
+    constexpr int NE = NMAX + 1;
+    constexpr int XS = PMAX * 32;
+    const double *xc = Xs + j * 32 + lane;
+    const double *rc = RX + j * 32 + lane;
+    const double bj = bget(b, j);
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i)
+        Ls[i * 32 + lane] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : ddiv(r[i], xc[i * XS]),
+                                 bj);  // np.divide then += b[j] (ccd.py:165-166)
+    // breakpoint i (Ls[NMAX] holds the lambda breakpoint's 0.0 from the kernel start)
+    auto loc = [&](int i) { return Ls[i * 32 + lane]; };
+    int m = cand[0];
+#pragma unroll
+    for (int k = 1; k < PMAX; ++k) m = (j == k) ? cand[k] : m;
+    const double tm = Ls[m * 32 + lane];
+    double wb = 0.0;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+        const double li = loc(i);
+        const bool below = (li < tm) | ((li == tm) & (i < m));
+        const double wi = i < NMAX ? fabs(xc[i * XS]) : lam;
+        if (below) wb = dadd(wb, wi);
+    }
+    const double wm = m < NMAX ? fabs(xc[(m < NMAX ? m : 0) * XS]) : lam;
+    const double total = Tw[j * 32 + lane];
+    const double half = dmul(0.5, total), marg = dmul(THREAD_MEDIAN_MARGIN, total);
+    double t_new;
+    if ((wb < dsub(half, marg)) & (dadd(wb, wm) > dadd(half, marg)) & (tm == tm)) {
+        t_new = tm;
+    } else {
+        const MedianPick mp = median_by_sort<NMAX, PMAX>(Ls, xc, lane, lam);
+        t_new = mp.t;
+#pragma unroll
+        for (int k = 0; k < PMAX; ++k) cand[k] = (j == k) ? mp.ik : cand[k];
+    }
+    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
+    const double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
+    const double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, loc(i))); },
+                                       [&](int i) { return i < NMAX ? fabs(xc[(i < NMAX ? i : 0) * XS]) : lam; });
+    const double v_new = dadd(constant, dot);
+    if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
+        const double delta = dsub(t_new, bj);
 #pragma unroll
         for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
         sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
@@ -1086,19 +1261,28 @@ __device__ __noinline__ void step_general(double *r, double *b, const double *Xs
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int NMAX, int PMAX>
+template <int NMAX, int PMAX, bool EXACT>
 __host__ __device__ constexpr size_t smem_doubles_per_warp()
 {
-    return (size_t)NMAX * PMAX * 32 + (size_t)NMAX * 32 + (size_t)(NMAX + 1) * 32;
+    return (size_t)NMAX * PMAX * 32 * (EXACT && LAD_THREAD_RCP ? 2 : 1) +
+           (EXACT && LAD_THREAD_YGLOBAL ? 0 : (size_t)NMAX * 32) + (size_t)(NMAX + 1) * 32 +
+           (EXACT && LAD_THREAD_CAND ? (size_t)PMAX * 32 : 0);
 }
 
-// Occupancy hint for the compile-time-shape kernel (config 1: n = 10, p = 2):
-// 18 one-warp blocks per SM caps it at 96 registers (21 resident warps instead
-// of 16 at 128).  The per-thread controller state lives in local memory and
-// misses L1 either way; more warps in flight hide more of it.  Same-box A/B:
-// +15.6% (hints 12 / 17 / 19 / 20 / 24: -1% / +14% / +14% / +13% / -1%).
+
+
+// Occupancy hint for the compile-time-shape kernel (config 1: n = 10, p = 2).
+// With the controller inlined, 10 one-warp blocks per SM (168 registers, 12
+// resident warps, no spills) beat a higher occupancy with spills: same-box A/B
+// at B = 262,144 (solves/s): 96 registers (20 warps) 6.19 M, 128 (16) 7.98 M,
+// hint 14 (128 registers) 8.14 M, hint 12 (167) 7.99 M, hint 10 (168) 8.30 M,
+// hint 8 (189) 7.18 M.  Also measured and rejected at this shape: the
+// reciprocal-table division (LAD_THREAD_RCP: more shared memory, 7.86 M), y
+// read from global memory (LAD_THREAD_YGLOBAL: 7.31 M at hint 12), a zero-
+// dividend bypass of the division's slow path (7.91 M), and the median guess
+// (LAD_THREAD_CAND: any lane's miss makes the whole warp sort; 5.2 M vs 5.9 M).
 #ifndef LAD_THREAD_MIN_BLOCKS
-#define LAD_THREAD_MIN_BLOCKS 18
+#define LAD_THREAD_MIN_BLOCKS 10
 #endif
 template <int NMAX, bool EXACT>
 constexpr int thread_min_blocks = (EXACT && NMAX <= 10) ? LAD_THREAD_MIN_BLOCKS : 1;
@@ -1108,9 +1292,13 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
 {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
+    constexpr bool ysh = !(EXACT && LAD_THREAD_YGLOBAL);  // y staged in shared memory
     double *Xs = smem;
-    double *Ys = Xs + NMAX * PMAX * 32;
-    double *Ls = Ys + NMAX * 32;
+    double *Ys = ysh ? Xs + NMAX * PMAX * 32 : nullptr;
+    double *Ls = Xs + NMAX * PMAX * 32 + (ysh ? NMAX * 32 : 0);
+    double *Tw = Ls + (NMAX + 1) * 32;                                // LAD_THREAD_CAND: PMAX * 32 doubles
+    double *RX = Tw + (EXACT && LAD_THREAD_CAND ? PMAX * 32 : 0);   // LAD_THREAD_RCP: NMAX * PMAX * 32 doubles
+    Ls[NMAX * 32 + lane] = 0.0;  // the lambda breakpoint's location
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = EXACT ? NMAX : A.n;
     const int p = EXACT ? PMAX : A.p;
@@ -1120,8 +1308,12 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
     C.pc = PC_FETCH;
     double r[NMAX];
     double b[PMAX];
+    int cand[PMAX];  // per axis: the element that was the weighted median at its last step (a guess)
 #pragma unroll
-    for (int k = 0; k < PMAX; ++k) b[k] = 0.0;
+    for (int k = 0; k < PMAX; ++k) {
+        b[k] = 0.0;
+        cand[k] = NMAX / 2;
+    }
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) r[i] = 0.0;
     double f_cur = 0.0, f_sweep_start = 0.0, sum_abs_b = 0.0, tol = 0.0, lam = 0.0;
@@ -1138,8 +1330,9 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
         __syncwarp();
         if (!__any_sync(0xffffffffu, alive)) break;
         if (alive && need_ctl) {
-            ThreadAccess<NMAX, PMAX> acc{n, p, lane, Xs, Ys};
-            int act = controller<PMAX>(C, A, acc, slot);
+            ThreadAccess<NMAX, PMAX> acc{n, p, lane, Xs, Ys, EXACT && LAD_THREAD_CAND ? Tw : nullptr,
+                                         EXACT && LAD_THREAD_RCP ? RX : nullptr};
+            int act = LAD_THREAD_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot) : controller<PMAX>(C, A, acc, slot);
             if (act == ACT_EXIT) {
                 alive = false;
             } else {
@@ -1156,7 +1349,7 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
                     if (i < n) {
                         double g = gemv_row(p, i, n, [&](int jj) { return Xs[i * XS + jj * 32 + lane]; },
                                             [&](int jj) { return b[jj < PMAX ? jj : PMAX - 1]; });
-                        r[i] = dsub(Ys[i * 32 + lane], g);
+                        r[i] = dsub(ysh ? Ys[i * 32 + lane] : __ldg(C.ysrc + i), g);
                     }
                 }
                 double sb = np_sum(p, [&](int jj) { return fabs(b[jj < PMAX ? jj : PMAX - 1]); });
@@ -1181,7 +1374,8 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
 #pragma unroll
                     for (int k = 0; k < PMAX; ++k)
                         if (k < p) C.res_beta[k] = b[k];
-                    C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+                    C.res_obj = objective_of<NMAX, PMAX>(Xs, ysh ? Ys + lane : C.ysrc, ysh ? 32 : 1, n, p, lane, lam,
+                                                         C.res_beta);
                     C.D += 1;
                     need_ctl = true;
                 }
@@ -1193,7 +1387,12 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
         bool dense_step = false;
         if constexpr (EXACT) {
             dense_step = !((sparse >> j) & 1u);
-            if (dense_step) step_dense<NMAX, PMAX>(r, b, Xs, Ls, lane, j, lam, f_cur, sum_abs_b);
+            if (dense_step) {
+                if constexpr (LAD_THREAD_CAND)
+                    step_dense_cand<NMAX, PMAX>(r, b, cand, Xs, RX, Ls, Tw, lane, j, lam, f_cur, sum_abs_b);
+                else
+                    step_dense<NMAX, PMAX>(r, b, Xs, RX, Ls, lane, j, lam, f_cur, sum_abs_b);
+            }
         }
         if (!dense_step) {
             // rare path (zero entries in column j, or runtime-shape kernel): work on
@@ -1237,7 +1436,8 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
 #pragma unroll
                 for (int k = 0; k < PMAX; ++k)
                     if (k < p) C.res_beta[k] = b[k];
-                C.res_obj = objective_of<NMAX, PMAX>(Xs, Ys, n, p, lane, lam, C.res_beta);
+                C.res_obj = objective_of<NMAX, PMAX>(Xs, ysh ? Ys + lane : C.ysrc, ysh ? 32 : 1, n, p, lane, lam,
+                                                     C.res_beta);
                 C.res_conv = conv;
                 C.res_sweeps = sweeps;
                 C.res_steps = steps;

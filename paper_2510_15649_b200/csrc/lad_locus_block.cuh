@@ -222,7 +222,7 @@ struct BlockAccess {
         for (int i = 0; i < n; ++i) s = dadd(s, fabs(M.X[i * p + j]));
         return s;
     }
-    __device__ double y_absmax() const
+    __device__ double y_absmax(const double *) const
     {
         double ymax = 0.0;
         for (int i = 0; i < n; ++i) {

@@ -282,7 +282,7 @@ struct WarpAccess {
         for (int i = 0; i < n; ++i) s = dadd(s, fabs(W->X[i * p + j]));
         return (double)s;
     }
-    __device__ double y_absmax() const
+    __device__ double y_absmax(const double *) const
     {
         T ymax = T(0);
         for (int i = 0; i < n; ++i) {

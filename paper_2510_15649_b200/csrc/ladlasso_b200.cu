@@ -83,7 +83,7 @@ struct Variant {
 template <int N, int P, bool EXACT>
 Variant make_thread_variant()
 {
-    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P>() * sizeof(double), 32, 32};
+    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P, EXACT>() * sizeof(double), 32, 32};
 }
 
 template <int P, int NC, typename T = double>
