@@ -209,8 +209,7 @@ __device__ double objective_of(const double *Xs, const double *Yp, int ys, int n
     do {                         \
         C.probe_t = (T);         \
         C.ret_pc = (RET);        \
-        C.pc = PC_PR_BEGIN;      \
-        goto next_state;         \
+        goto L_PC_PR_BEGIN;      \
     } while (0)
 
 template <int PMAX>
@@ -407,7 +406,10 @@ struct ThreadAccess {
 // the nearest-seen-point scan, and which thread writes shared results.  The
 // controller itself is the same for the thread-per-problem and the
 // warp-per-problem kernels (in the latter all 32 lanes run it in lock-step
-// on a shared Ctl, with identical values).
+// on a shared Ctl, with identical values).  C.pc is the state to resume at
+// after a descent (set by ISSUE) and after a probe (ret_pc); every other
+// transition is a direct jump to the next state's label, not a round trip
+// through the state switch.
 template <int PMAX, class AC>
 __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A, const AC &acc, int slot)
 {
@@ -417,6 +419,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
     for (;;) {
         acc.sync();
         switch (C.pc) {
+        L_PC_FETCH:
         case PC_FETCH: {
             int got = acc.fetch(C, A);
             if (got < 0) return ACT_EXIT;
@@ -424,7 +427,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.S = 0;
             C.replay = 0;
             C.seen_over = 0;
-            if (got == 0) continue;  // invalid problem: status written, fetch the next one
+            if (got == 0) goto L_PC_FETCH;  // invalid problem: status written, fetch the next one
             const int64_t pr = C.prob;
             if (A.mode == MODE_DESCENT) {
                 const double *st = A.start + (size_t)pr * p;
@@ -458,8 +461,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 const double blo = A.brackets[2 * pr], bhi = A.brackets[2 * pr + 1];
                 if (!(isfinite(blo) && isfinite(bhi) && blo < bhi)) {
                     if (acc.leader()) write_invalid<PMAX>(A, pr, p);
-                    C.pc = PC_FETCH;
-                    continue;
+                    goto L_PC_FETCH;
                 }
                 C.R_lo = blo;
                 C.R_hi = bhi;
@@ -479,16 +481,14 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.outer_ok = 1;
             C.confirmations = 0;
             if (A.axis_mode == AXIS_SEARCH) {  // this item is one axis search of the problem
-                if (C.arank >= C.naxes) continue;
+                if (C.arank >= C.naxes) goto L_PC_FETCH;
                 C.a_idx = C.arank;
-                C.pc = PC_AXIS_START;
-            } else {
-                C.pc = PC_AXIS_START;
             }
-            break;
+            goto L_PC_AXIS_START;
         }
         // axis-parallel finish: replay the stored per-axis results in influence
         // order through the same agreement rule (locus.py:338-362)
+        L_PC_FINISH_AXES:
         case PC_FINISH_AXES: {
             // written by other warps of this launch (fused finish): read through L2
             const double *res = A.axis_res + ((size_t)C.prob * p + C.a_idx) * A.axis_stride;
@@ -506,22 +506,20 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.S += (long long)__ldcg(res + 8 + PMAX);
             if (C.oconv < 0) {  // this axis' bracket expansion failed: raise here, as the serial scan does
                 write_unbounded<PMAX>(A, C, p, acc.leader());
-                C.pc = PC_FETCH;
-                break;
+                goto L_PC_FETCH;
             }
-            C.pc = PC_AXIS_DONE;
-            break;
+            goto L_PC_AXIS_DONE;
         }
         // The unit that completes a problem's last axis search replays all of
         // them through the agreement rule, refine and polish right away: the
         // finish of one problem overlaps the other problems' searches, and the
         // problem is still loaded.  Same states as a separate finish pass.
+        L_PC_AXIS_COUNT:
         case PC_AXIS_COUNT: {
             const bool last = acc.last_of(A.axis_done + C.prob, (unsigned)C.naxes);
             acc.sync();
             if (!last) {
-                C.pc = PC_FETCH;
-                break;
+                goto L_PC_FETCH;
             }
             C.replay = 1;
             C.a_idx = 0;
@@ -532,9 +530,8 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.D = 0;  // the replay adds every axis' D and S
             C.S = 0;
             C.seen_over = 0;
-            C.pc = PC_FINISH_AXES;
             acc.sync();
-            break;
+            goto L_PC_FINISH_AXES;
         }
         case PC_DESC_AFTER: {
             int64_t pr = C.prob;
@@ -548,21 +545,22 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             if (A.descents) A.descents[pr] = C.D;
             if (A.steps) A.steps[pr] = C.S;
             }
-            C.pc = PC_FETCH;
-            break;
+            goto L_PC_FETCH;
         }
         // ------------------------------------------------ axis search
+        L_PC_AXIS_START:
         case PC_AXIS_START: {
             evaluator_reset(C, C.axes[C.a_idx], A, p);
             C.lo = C.R_lo;
             C.hi = C.R_hi;
-            C.pc = PC_EX_0;
-            break;
+            goto L_PC_EX_0;
         }
         // expand_bracket (linesearch.py:247-268)
+        L_PC_EX_0:
         case PC_EX_0: PROBE(C.lo, PC_EX_1);
         case PC_EX_1: C.g_lo = C.probe_v; PROBE(C.hi, PC_EX_2);
-        case PC_EX_2: C.g_hi = C.probe_v; C.ex_it = 0; C.pc = PC_EX_LOOP; break;
+        case PC_EX_2: C.g_hi = C.probe_v; C.ex_it = 0; goto L_PC_EX_LOOP;
+        L_PC_EX_LOOP:
         case PC_EX_LOOP: {
             if (C.ex_it >= 60) {  // UnboundedDirectionError (linesearch.py:266)
                 if (A.axis_mode == AXIS_SEARCH && !C.replay) {
@@ -574,20 +572,17 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                         res[8 + PMAX] = (double)C.S;
                         res[9 + PMAX] = C.seen_over;
                     }
-                    C.pc = PC_AXIS_COUNT;
-                    break;
+                    goto L_PC_AXIS_COUNT;
                 }
                 write_unbounded<PMAX>(A, C, p, acc.leader());
-                C.pc = PC_FETCH;
-                break;
+                goto L_PC_FETCH;
             }
             PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_EX_MID);
         }
         case PC_EX_MID: {
             double g_mid = C.probe_v;
             if (g_mid < C.g_lo && g_mid < C.g_hi) {
-                C.pc = PC_OT_START;
-                break;
+                goto L_PC_OT_START;
             }
             double step = dmul(1.0, dsub(C.hi, C.lo));
             if (C.g_lo < C.g_hi) {
@@ -602,16 +597,18 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 PROBE(C.lo, PC_EX_BOTH1);
             }
         }
-        case PC_EX_NEWLO: C.g_lo = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
-        case PC_EX_NEWHI: C.g_hi = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
+        case PC_EX_NEWLO: C.g_lo = C.probe_v; C.ex_it++; goto L_PC_EX_LOOP;
+        case PC_EX_NEWHI: C.g_hi = C.probe_v; C.ex_it++; goto L_PC_EX_LOOP;
         case PC_EX_BOTH1: C.g_lo = C.probe_v; PROBE(C.hi, PC_EX_BOTH2);
-        case PC_EX_BOTH2: C.g_hi = C.probe_v; C.ex_it++; C.pc = PC_EX_LOOP; break;
+        case PC_EX_BOTH2: C.g_hi = C.probe_v; C.ex_it++; goto L_PC_EX_LOOP;
         // ternary_min / quadrature_min (linesearch.py:172-233)
+        L_PC_OT_START:
         case PC_OT_START: {
             C.target = dmul(A.prm.outer_tolerance, dsub(C.hi, C.lo));
             C.orounds = 0;
             PROBE(dmul(0.5, dadd(C.lo, C.hi)), A.prm.outer_search == 0 ? PC_OT_LOOP : PC_OQ_LOOP);
         }
+        L_PC_OT_LOOP:
         case PC_OT_LOOP: {
             if (dsub(C.hi, C.lo) > C.target && C.orounds < A.prm.outer_max_iterations) {
                 double third = ddiv(dsub(C.hi, C.lo), 3.0);
@@ -626,9 +623,9 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             if (C.v1 < C.probe_v) C.hi = C.m2;
             else C.lo = C.m1;
             C.orounds++;
-            C.pc = PC_OT_LOOP;
-            break;
+            goto L_PC_OT_LOOP;
         }
+        L_PC_OQ_LOOP:
         case PC_OQ_LOOP: {
             if (dsub(C.hi, C.lo) > C.target && C.orounds < A.prm.outer_max_iterations) {
                 C.h = ddiv(dsub(C.hi, C.lo), (double)(A.prm.outer_probes + 1));
@@ -649,15 +646,14 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.lo = nlo > C.lo ? nlo : C.lo;
             C.hi = nhi < C.hi ? nhi : C.hi;
             C.orounds++;
-            C.pc = PC_OQ_LOOP;
-            break;
+            goto L_PC_OQ_LOOP;
         }
         case PC_OUTER_END: {
             C.oconv = dsub(C.hi, C.lo) <= C.target;
-            C.pc = PC_AXIS_DONE;
-            break;
+            goto L_PC_AXIS_DONE;
         }
         // axis agreement bookkeeping (locus.py:338-362)
+        L_PC_AXIS_DONE:
         case PC_AXIS_DONE: {
             if (A.axis_mode == AXIS_SEARCH && !C.replay) {  // store this axis' result; the finish combines them
                 if (acc.leader()) {
@@ -674,8 +670,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                     res[8 + PMAX] = (double)C.S;
                     res[9 + PMAX] = C.seen_over;
                 }
-                C.pc = PC_AXIS_COUNT;
-                break;
+                goto L_PC_AXIS_COUNT;
             }
             Point<PMAX> &ab = C.ev_best;
             C.axis_values[C.nvals++] = ab.value;
@@ -698,15 +693,15 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             if (p > 3 && C.confirmations >= 2) brk = true;
             C.a_idx++;
-            C.pc = (brk || C.a_idx >= C.naxes) ? PC_REFINE_START
-                                                : (A.axis_mode != AXIS_SERIAL ? PC_FINISH_AXES : PC_AXIS_START);
-            break;
+            if (brk || C.a_idx >= C.naxes) goto L_PC_REFINE_START;
+            if (A.axis_mode != AXIS_SERIAL) goto L_PC_FINISH_AXES;
+            goto L_PC_AXIS_START;
         }
         // dense refinement plan (locus.py:363-395)
+        L_PC_REFINE_START:
         case PC_REFINE_START: {
             if (p <= 2) {
-                C.pc = PC_POLISH;
-                break;
+                goto L_PC_POLISH;
             }
             C.width = dmul(0.01, dsub(C.R_hi, C.R_lo));
             double vmax = C.axis_values[0], vmin = C.axis_values[0];
@@ -730,9 +725,9 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.ps = 0;
             C.q = 0;
             C.improved = 0;
-            C.pc = PC_REF_AXIS_START;
-            break;
+            goto L_PC_REF_AXIS_START;
         }
+        L_PC_REF_AXIS_START:
         case PC_REF_AXIS_START: {
             int axis = C.refine_axes[C.q];
             evaluator_reset(C, axis, A, p);
@@ -745,9 +740,9 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.margin = dmul(C.margin_scale, fmax(1.0, fabs(C.seeded.value)));
             C.rng.seed(0x5EEDULL + (uint64_t)axis, 54);
             C.fan_i = 0;
-            C.pc = PC_REF_FAN;
-            break;
+            goto L_PC_REF_FAN;
         }
+        L_PC_REF_FAN:
         case PC_REF_FAN: {
             if (C.fan_i < C.fan) {
                 double st[PMAX];
@@ -763,8 +758,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             C.w = C.width;
             C.rr = 0;
-            C.pc = PC_REF_ROUND;
-            break;
+            goto L_PC_REF_ROUND;
         }
         case PC_REF_FAN_AFTER: {
             set_point_from_result(C, C.pt, C.seeded.t, p);
@@ -772,22 +766,21 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 double tt = C.seeded.t;
                 ISSUE(jj_ == C.axis ? tt : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_REF_FAN_REFINED);
             }
-            C.pc = PC_REF_FAN_FINISH;
-            break;
+            goto L_PC_REF_FAN_FINISH;
         }
         case PC_REF_FAN_REFINED: {
             if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.seeded.t, p);
-            C.pc = PC_REF_FAN_FINISH;
-            break;
+            goto L_PC_REF_FAN_FINISH;
         }
+        L_PC_REF_FAN_FINISH:
         case PC_REF_FAN_FINISH: {
             C.ev_calls++;
             seen_append(A, seen, C, C.pt, p, acc.leader());
             if (C.pt.value < C.ev_best.value) C.ev_best = C.pt;
             C.fan_i++;
-            C.pc = PC_REF_FAN;
-            break;
+            goto L_PC_REF_FAN;
         }
+        L_PC_REF_ROUND:
         case PC_REF_ROUND: {
             if (C.rr < 4) {
                 double center = C.ev_best.t;
@@ -799,8 +792,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 PROBE(C.gstep == 0.0 ? dadd(dmul(ddiv(0.0, 15.0), C.gdelta), C.ga) : dadd(dmul(0.0, C.gstep), C.ga),
                       PC_REF_GRID_NEXT);
             }
-            C.pc = PC_REF_AXIS_DONE;
-            break;
+            goto L_PC_REF_AXIS_DONE;
         }
         case PC_REF_GRID_NEXT: {
             C.gk++;
@@ -813,9 +805,9 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             C.w = dmul(C.w, 2.0 / 15.0);
             C.rr++;
-            C.pc = PC_REF_ROUND;
-            break;
+            goto L_PC_REF_ROUND;
         }
+        L_PC_REF_AXIS_DONE:
         case PC_REF_AXIS_DONE: {
             Point<PMAX> &cand = C.ev_best;
             C.calls += C.ev_calls;
@@ -824,20 +816,18 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             if (cand.value < C.best.value) C.best = cand;
             C.q++;
             if (C.q < C.nref) {
-                C.pc = PC_REF_AXIS_START;
-                break;
+                goto L_PC_REF_AXIS_START;
             }
             C.ps++;
             if (!C.improved || C.ps >= C.passes) {
-                C.pc = PC_POLISH;
-                break;
+                goto L_PC_POLISH;
             }
             C.q = 0;
             C.improved = 0;
-            C.pc = PC_REF_AXIS_START;
-            break;
+            goto L_PC_REF_AXIS_START;
         }
         // final snap (locus.py:396-409)
+        L_PC_POLISH:
         case PC_POLISH:
             ISSUE(C.best.beta[jj_], -1, A.prm.inner_sweep_tol, A.prm.inner_max_sweeps, PC_POLISH_AFTER);
         case PC_POLISH_AFTER: {
@@ -852,8 +842,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                     if (A.descents) A.descents[pr] = C.D;
                     if (A.steps) A.steps[pr] = C.S;
                 }
-                C.pc = PC_FETCH;
-                break;
+                goto L_PC_FETCH;
             }
             if (acc.leader()) {
             for (int j = 0; j < p; ++j) A.beta[(size_t)pr * p + j] = use_pol ? C.res_beta[j] : C.best.beta[j];
@@ -865,10 +854,10 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             if (A.descents) A.descents[pr] = C.D;
             if (A.steps) A.steps[pr] = C.S;
             }
-            C.pc = PC_FETCH;
-            break;
+            goto L_PC_FETCH;
         }
         // ------------------------------------------------ curve evaluator call
+        L_PC_PR_BEGIN:
         case PC_PR_BEGIN: {
             double t = C.probe_t;
             int wi = -1;
@@ -886,19 +875,17 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 double t = C.probe_t;
                 ISSUE(jj_ == C.axis ? t : wb[jj_], C.axis, C.fast_tol, C.fast_sweeps, PC_PR_AFTER_WARM);
             }
-            C.pc = PC_PR_REFINE_CHECK;
-            break;
+            goto L_PC_PR_REFINE_CHECK;
         }
         case PC_PR_AFTER_WARM: {
             if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
-            C.pc = PC_PR_REFINE_CHECK;
-            break;
+            goto L_PC_PR_REFINE_CHECK;
         }
         case PC_PR_AFTER_FAST_ONLY: {
             set_point_from_result(C, C.pt, C.probe_t, p);
-            C.pc = PC_PR_REFINE_CHECK;
-            break;
+            goto L_PC_PR_REFINE_CHECK;
         }
+        L_PC_PR_REFINE_CHECK:
         case PC_PR_REFINE_CHECK: {
             bool refine = !C.has_best ||
                           C.pt.value <= dadd(C.ev_best.value, dmul(C.margin_scale, fmax(1.0, fabs(C.ev_best.value))));
@@ -906,14 +893,13 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 double t = C.probe_t;
                 ISSUE(jj_ == C.axis ? t : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_PR_AFTER_REFINE);
             }
-            C.pc = PC_PR_FINISH;
-            break;
+            goto L_PC_PR_FINISH;
         }
         case PC_PR_AFTER_REFINE: {
             if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
-            C.pc = PC_PR_FINISH;
-            break;
+            goto L_PC_PR_FINISH;
         }
+        L_PC_PR_FINISH:
         case PC_PR_FINISH: {
             C.ev_calls++;
             C.ev_failures += C.pt.conv ? 0 : 1;
@@ -923,13 +909,12 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 C.has_best = 1;
             }
             C.probe_v = C.pt.value;
-            C.pc = C.ret_pc;
+            C.pc = C.ret_pc;  // the probe's caller: the one dynamic transition (through the switch)
             break;
         }
         default:
             return ACT_EXIT;
         }
-    next_state:;
     }
 }
 

@@ -58,6 +58,53 @@ constexpr int warps_per_block = (PMAX <= 5 || sizeof(T) == 4) ? LAD_WARP_WARPS_N
 template <int PMAX, typename T>
 constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5;
 
+// Pad rows as data (with the reciprocal table): row n of X holds lambda and
+// rows > n hold 0, and the pad lanes' residual stays 1, so every lane's
+// breakpoint weight is |x_ij| and every lane divides r / x without the pad
+// selects (a pad lane's quotient is finite and discarded).
+#ifndef LAD_WARP_PADX
+#define LAD_WARP_PADX 1
+#endif
+template <int PMAX, typename T>
+constexpr bool padx_v = LAD_WARP_PADX && fast_div_v<PMAX, T>;
+// Descent loop specialised for problems without sparse columns (compile-time
+// n kernels), optionally with the sweep over the axes unrolled.
+#ifndef LAD_WARP_DENSE_LOOP
+#define LAD_WARP_DENSE_LOOP 1
+#endif
+#ifndef LAD_WARP_UNROLL
+#define LAD_WARP_UNROLL 0
+#endif
+// Step micro-variants (same-box A/B): the through-weight of the median guess
+// as the below-weight plus its own weight (a shuffle instead of a second
+// REDUX); the margin bounds (half -+ margin) precomputed per axis (one
+// 64-bit load instead of load + REDUX + two adds); the walk's neighbour from
+// the high key word alone when it is unique (one REDUX per hop instead of
+// two); the ddot lane tree from products staged in shared memory (no
+// shuffles).
+#ifndef LAD_WARP_QI_SHFL
+#define LAD_WARP_QI_SHFL 0
+#endif
+#ifndef LAD_WARP_HQ_PAIR
+#define LAD_WARP_HQ_PAIR 1
+#endif
+#ifndef LAD_WARP_WALK_POPC
+#define LAD_WARP_WALK_POPC 0
+#endif
+#ifndef LAD_WARP_DDOT_SMEM
+#define LAD_WARP_DDOT_SMEM 0
+#endif
+// Controller inlined into the warp kernel's outer loop (warp_descent stays out
+// of line).
+#ifndef LAD_WARP_INLINE_CTL
+#define LAD_WARP_INLINE_CTL 1
+#endif
+// The median test's half-total weight by a broadcast load (1 instruction)
+// instead of a REDUX into a uniform register.
+#ifndef LAD_WARP_HQ_LDS
+#define LAD_WARP_HQ_LDS 0
+#endif
+
 template <int PMAX, typename T>
 struct WarpShared {
     using T2 = typename vec2_of<T>::type;
@@ -72,6 +119,8 @@ struct WarpShared {
     int cand[PMAX];      // per axis: element that was the weighted median last time (a guess)
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
+    uint2 hqb[PMAX];        // per axis: (halfq - margin (0 if below), halfq + margin)
+    alignas(16) T pp[32];   // ddot lane-tree products, lane l's four at [4 l, 4 l + 4) (n1 = 16) / [8 l, 8 l + 8)
 };
 
 // margin of the fixed-point median test, in units of 2^-30 of the total weight
@@ -101,6 +150,11 @@ struct OrderKey<double> {
         const unsigned h = after ? hi : ~hi, l = after ? lo : ~lo;
         const unsigned mh = __reduce_min_sync(FULLMASK, side ? h : ~0u);
         const bool c1 = side && h == mh;
+        if constexpr (LAD_WARP_WALK_POPC) {  // a unique high word decides (no side lane has h = ~0)
+            const unsigned b1 = __ballot_sync(FULLMASK, c1);
+            if (b1 == 0u) return -1;
+            if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+        }
         const unsigned ml = __reduce_min_sync(FULLMASK, c1 ? l : ~0u);
         const unsigned bal = __ballot_sync(FULLMASK, c1 && l == ml);
         if (bal == 0u) return -1;
@@ -249,6 +303,8 @@ struct WarpAccess {
         else lraw = A.lam[pr];
         ok = ok && isfinite(lraw) && lraw >= 0.0;
         const double lam_eff = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
+        if constexpr (padx_v<PMAX, T>)  // row n: the lambda breakpoint's weight; rows > n: weight 0
+            for (int e = n * p + lane; e < 32 * p; e += 32) W->X[e] = e < (n + 1) * p ? T(lam_eff) : T(0);
         __syncwarp();
         // fixed-point breakpoint weights of each axis (median fast path): any
         // summation order will do, the test keeps a margin of 2^14 units
@@ -261,7 +317,11 @@ struct WarpAccess {
             const unsigned q = (tot > 0.0 && tot < 1e300) ? __double2uint_rz(wd * scale) : 0u;
             W->wq[j][lane] = q;
             const unsigned sq = __reduce_add_sync(FULLMASK, q);
-            if (lane == 0) W->halfq[j] = sq / 2u;
+            if (lane == 0) {
+                const unsigned hq = sq / 2u;
+                W->halfq[j] = hq;
+                W->hqb[j] = make_uint2(hq >= MEDIAN_MARGIN_Q ? hq - MEDIAN_MARGIN_Q : 0u, hq + MEDIAN_MARGIN_Q);
+            }
         }
         C.prob = (int64_t)pr;
         C.arank = (int)(item % div);
@@ -479,24 +539,37 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     bool hit = false;
     if (cacheable) {
         const unsigned q = W->wq[j][lane];
-        const unsigned hq = __reduce_max_sync(FULLMASK, W->halfq[j]);  // uniform register
+        // margin bounds: element m is the median iff qb < lo_b and qi > hi_b
+        unsigned lo_b, hi_b;
+        if constexpr (LAD_WARP_HQ_PAIR) {
+            const uint2 hb = W->hqb[j];
+            lo_b = hb.x;
+            hi_b = hb.y;
+        } else {
+            const unsigned hq = LAD_WARP_HQ_LDS ? W->halfq[j] : __reduce_max_sync(FULLMASK, W->halfq[j]);
+            lo_b = hq >= MEDIAN_MARGIN_Q ? hq - MEDIAN_MARGIN_Q : 0u;
+            hi_b = hq + MEDIAN_MARGIN_Q;
+        }
         const int m1 = W->cand[j];
         // Where is element m relative to the median, given the fixed-point
         // weight before it (qb) and through it (qi)?  0: m is the median; +1:
         // the median comes after m, -1: before m (decided beyond the margin);
         // 2: undecided.  Exact integer sums: the answer is warp-uniform.
+        // (qb < half - margin  <=>  qb + margin < half, for half >= margin;
+        // lo_b = 0 otherwise, where nothing is decided below.)
         auto verdict = [&](unsigned qb, unsigned qi) {
-            if ((qb + MEDIAN_MARGIN_Q < hq) & (qi > hq + MEDIAN_MARGIN_Q)) return 0;
-            if (qi + MEDIAN_MARGIN_Q < hq) return 1;
-            if (qb > hq + MEDIAN_MARGIN_Q) return -1;
+            if ((qb < lo_b) & (qi > hi_b)) return 0;
+            if (qi < lo_b) return 1;
+            if (qb > hi_b) return -1;
             return 2;
         };
         // first candidate (the hit path: ~83% of config-2 steps decide here)
         t_new = shfl_t(loc, m1);
         const bool below1 = (loc < t_new) | ((loc == t_new) & (lane < m1));
         const unsigned qb1 = __reduce_add_sync(FULLMASK, below1 ? q : 0u);
-        const unsigned qi1 = __reduce_add_sync(FULLMASK, (below1 | (lane == m1)) ? q : 0u);
-        hit = (qb1 + MEDIAN_MARGIN_Q < hq) & (qi1 > hq + MEDIAN_MARGIN_Q);
+        const unsigned qi1 = LAD_WARP_QI_SHFL ? qb1 + __shfl_sync(FULLMASK, q, m1)
+                                              : __reduce_add_sync(FULLMASK, (below1 | (lane == m1)) ? q : 0u);
+        hit = (qb1 < lo_b) & (qi1 > hi_b);
         if (!hit) {
             const int v1 = verdict(qb1, qi1);
             // Walk from m1 towards the median through its neighbours in the
@@ -565,7 +638,29 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     // and go through shared memory, where every lane folds (S0 + S2) + (S1 + S3)
     // itself (one store/load instead of three dependent shuffle rounds).
     T *const sl = reinterpret_cast<T *>(W->sl);
-    if (n1 == 16) {
+    if constexpr (LAD_WARP_DDOT_SMEM) {
+        // products staged so that lane l < 4 finds its partial sum's terms
+        // contiguous: n1 = 16: p_{l + 4k} at 4 l + k; n1 = 32: p_{8k + l + 4h} at 8 l + 2 k + h
+        if (n1 == 16) {
+            if (lane < 16) W->pp[(lane & 3) * 4 + (lane >> 2)] = pr;
+        } else if (n1 == 32) {
+            W->pp[(lane & 3) * 8 + (lane >> 3) * 2 + ((lane >> 2) & 1)] = pr;
+        }
+        W->aw[lane] = {a, wv};  // FMA tail operands as (a, w) pairs
+        __syncwarp();
+        if (lane < 4) {
+            using T2 = typename vec2_of<T>::type;
+            if (n1 == 16) {
+                const T2 *pl = reinterpret_cast<const T2 *>(W->pp) + 2 * lane;
+                const T2 u = pl[0], v = pl[1];
+                sl[lane] = dadd(dadd(dadd(u.x, u.y), v.x), v.y);
+            } else if (n1 == 32) {
+                const T2 *pl = reinterpret_cast<const T2 *>(W->pp) + 4 * lane;
+                const T2 a0 = pl[0], a1 = pl[1], a2 = pl[2], a3 = pl[3];
+                sl[lane] = dadd(dadd(dadd(dadd(a0.x, a0.y), dadd(a1.x, a1.y)), dadd(a2.x, a2.y)), dadd(a3.x, a3.y));
+            }
+        }
+    } else if (n1 == 16) {
         const T q4 = shfl_down_t(pr, 4), q8 = shfl_down_t(pr, 8), q12 = shfl_down_t(pr, 12);
         const T S = dadd(dadd(dadd(pr, q4), q8), q12);
         if (lane < 4) sl[lane] = S;
@@ -575,7 +670,7 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
         const T S = dadd(dadd(dadd(A2, a8), a16), a24);
         if (lane < 4) sl[lane] = S;
     }
-    W->aw[lane] = {a, wv};  // FMA tail operands as (a, w) pairs
+    if constexpr (!LAD_WARP_DDOT_SMEM) W->aw[lane] = {a, wv};  // FMA tail operands as (a, w) pairs
     __syncwarp();
     T dot = T(0);
     if (n1 > 0) {
@@ -635,7 +730,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
     if (!col_sparse) {
         // np.divide then += b[j] (ccd.py:165-166).  Pad lanes divide 1/1 (their
         // result is discarded; it keeps them off the division's slow path).
-        const T rr = row ? r : T(1), xx = row ? xij : T(1);
+        const T rr = (padx_v<PMAX, T> || row) ? r : T(1), xx = (padx_v<PMAX, T> || row) ? xij : T(1);
         T q;
         if constexpr (fast_div_v<PMAX, T>) {
             q = div_by_rcp(rr, xx, yrow[j]);  // y = 1 on pad lanes
@@ -643,7 +738,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
             q = ddiv(rr, xx);
         }
         const T loc = row ? dadd(q, bj) : (lane == n ? T(0) : INF);
-        const T w = row ? fabs(xij) : (lane == n ? lam : T(0));
+        const T w = (padx_v<PMAX, T> || row) ? fabs(xij) : (lane == n ? lam : T(0));
         median_update<PMAX, (NC > 0 ? NC + 1 : 0), T>(W, lane, inv_mask, j, lam, true, n + 1, loc, w, T(0), false,
                                                       row, xij, bj, r, f_cur, sum_abs_b);
     } else if constexpr (PMAX <= 5) {
@@ -674,8 +769,16 @@ __device__ __forceinline__ T warp_objective(WarpShared<PMAX, T> *W, int lane, in
 }
 
 // ccd_descend (ccd.py:126-206) for the descent request in C, all lanes.
+#ifndef LAD_WARP_INLINE_DESC
+#define LAD_WARP_INLINE_DESC 1
+#endif
+#if LAD_WARP_INLINE_DESC
+#define LAD_WARP_DESC_ATTR __forceinline__
+#else
+#define LAD_WARP_DESC_ATTR __noinline__
+#endif
 template <int PMAX, int NC, typename T>
-__device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
+__device__ LAD_WARP_DESC_ATTR void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
                                           int p_rt)
 {
     const int n = NC > 0 ? NC : n_rt;
@@ -687,7 +790,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
     const uint32_t sparse = C.sparse_mask;
     if (lane < p) W->B[lane] = T(C.req_start[lane]);
     __syncwarp();
-    T r = T(0);
+    T r = padx_v<PMAX, T> ? T(1) : T(0);  // pad lanes (padx: a safe dividend that never changes)
     if (lane < n) {
         T g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * p + q]; }, [&](int q) { return W->B[q]; });
         r = dsub(W->Y[lane], g);
@@ -702,6 +805,34 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
     int j = j0;
     if (j >= p) {
         conv = 1;
+    } else if (LAD_WARP_DENSE_LOOP && NC > 0 && sparse == 0u) {
+        // Every column dense (the common case): no per-step sparse test, and with
+        // LAD_WARP_UNROLL the sweep over the PMAX axes is unrolled (compile-time
+        // axis offsets, no axis bookkeeping); the frozen axis is skipped in place.
+        for (;;) {
+            if constexpr (LAD_WARP_UNROLL) {
+#pragma unroll
+                for (int jj = 0; jj < PMAX; ++jj) {
+                    if (jj == frozen) continue;
+                    warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, jj, lam, false, r, f_cur, sum_abs_b);
+                    ++steps;
+                }
+            } else {
+#pragma unroll 1
+                for (int jj = j0; jj < PMAX; jj += 1 + (jj + 1 == frozen)) {
+                    warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, jj, lam, false, r, f_cur, sum_abs_b);
+                    ++steps;
+                }
+            }
+            if (dsub(f_sweep_start, f_cur) < tol) {  // gain in T, compared in binary64
+                conv = 1;
+                break;
+            }
+            if (sweeps >= max_sweeps) break;
+            ++sweeps;
+            f_sweep_start = f_cur;
+            sum_abs_b = np_sum(p, [&](int q) { return fabs(W->B[q]); });
+        }
     } else {
         for (;;) {
             warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, j, lam, (sparse >> j) & 1u, r, f_cur,
@@ -759,7 +890,9 @@ __global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS
     if (lane == 0) C.pc = PC_FETCH;
     __syncwarp();
     for (;;) {
-        int act = controller<PMAX>(C, A, acc, slot);
+        // inlined: the controller reads LocusArgs straight from the kernel's parameter
+        // (constant) bank; out of line it reads every field from a per-lane stack copy
+        int act = LAD_WARP_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot) : controller<PMAX>(C, A, acc, slot);
         __syncwarp();
         if (act == ACT_EXIT) break;
         warp_descent<PMAX, NC, T>(W, C, lane, inv_mask, n, p);

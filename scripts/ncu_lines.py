@@ -28,6 +28,7 @@ nxt = sec.find("//---------------------", 10)
 sec = sec[:nxt] if nxt > 0 else sec
 where = {}
 chain_of = {}
+text_of = {}
 cur = ("?", 0)
 chain = []
 pending = []
@@ -38,8 +39,9 @@ for line in sec.splitlines():
         fr += [(os.path.basename(a), int(b)) for a, b in re.findall(r'inlined at "([^"]+)", line (\d+)', m.group(3))]
         pending.append(fr)
         continue
-    m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", line)
+    m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s*(.*?);", line)
     if m:
+        text_of[int(m.group(1), 16)] = m.group(2).strip()
         if pending:
             chain = max(pending, key=len)  # the innermost entry carries the full inline chain
             cur = chain[0]
@@ -74,5 +76,11 @@ if "--buckets" in sys.argv:
         print(f"  bucket {nm:14s} {n / per:8.2f} per unit  {100 * n / tot:5.1f}%")
     for ch, n in shown.most_common(25):
         print(f"    {n / per:7.2f}  " + " <- ".join(f"{f}:{l}" for f, l in ch))
+if "--sass-top" in sys.argv:  # the hottest SASS instructions: offset, count per unit, source line, text
+    nsass = int(sys.argv[sys.argv.index("--sass-top") + 1])
+    for a, n, smp in sorted(data, key=lambda x: -x[1])[:nsass]:
+        off = a - base
+        f, l = where.get(off, ("?", 0))
+        print(f"  sass {off:#08x} {n / per:7.3f} samples {smp:7.0f}  {f}:{l}  {text_of.get(off, '?')}")
 for (f, l), n in acc.most_common(top):
     print(f"{n / per:8.2f} {100 * n / tot:5.1f}%  stall-samples {stall[(f, l)]:8.0f}  {f}:{l}")
