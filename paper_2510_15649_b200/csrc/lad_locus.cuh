@@ -957,6 +957,26 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 #define LAD_THREAD_YGLOBAL 0
 #endif
 
+// r / x for the thread kernel's breakpoints (LAD_THREAD_ZDIV).  A residual is
+// often exactly 0 (the median row of an accepted step), and __ddiv_rn sends a
+// zero dividend down its full-range slow path (a call of ~60 instructions,
+// divergent: in a thread-per-problem warp some lane hits it at most steps);
+// 0 / x is the signed zero 0 * x for finite nonzero x, so a zero dividend
+// divides 1 instead and takes 0 * x.
+#ifndef LAD_THREAD_ZDIV
+#define LAD_THREAD_ZDIV 0
+#endif
+__device__ __forceinline__ double div_thread(double r, double x)
+{
+    if constexpr (LAD_THREAD_ZDIV) {
+        const bool z = (r == 0.0);
+        const double q = ddiv(z ? 1.0 : r, x);
+        return z ? dmul(r, x) : q;
+    } else {
+        return ddiv(r, x);
+    }
+}
+
 // beta register array accessed with a runtime axis index (select chains, no
 // local memory)
 template <int PMAX>
@@ -990,7 +1010,7 @@ __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX],
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
         // np.divide then += b[j] (ccd.py:165-166)
-        double loc = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : ddiv(r[i], xc[i * XS]), bj);
+        double loc = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : div_thread(r[i], xc[i * XS]), bj);
         key[i] = loc;
         idx[i] = i;
         Ls[i * 32 + lane] = loc;
@@ -1130,7 +1150,7 @@ __device__ __forceinline__ void step_dense_cand(double (&r)[NMAX], double (&b)[P
     const double bj = bget(b, j);
 #pragma unroll
     for (int i = 0; i < NMAX; ++i)
-        Ls[i * 32 + lane] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : ddiv(r[i], xc[i * XS]),
+        Ls[i * 32 + lane] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : div_thread(r[i], xc[i * XS]),
                                  bj);  // np.divide then += b[j] (ccd.py:165-166)
     // breakpoint i (Ls[NMAX] holds the lambda breakpoint's 0.0 from the kernel start)
     auto loc = [&](int i) { return Ls[i * 32 + lane]; };

@@ -94,6 +94,14 @@ constexpr bool padx_v = LAD_WARP_PADX && fast_div_v<PMAX, T>;
 #ifndef LAD_WARP_DDOT_SMEM
 #define LAD_WARP_DDOT_SMEM 0
 #endif
+// Dense descent loop over a packed list of the free axes (no per-step axis
+// bookkeeping); ddot tail operands stored signed with |.| folded into DFMA.
+#ifndef LAD_WARP_AXIS_LIST
+#define LAD_WARP_AXIS_LIST 0
+#endif
+#ifndef LAD_WARP_RAW_AW
+#define LAD_WARP_RAW_AW 0
+#endif
 // Controller inlined into the warp kernel's outer loop (warp_descent stays out
 // of line).
 #ifndef LAD_WARP_INLINE_CTL
@@ -670,7 +678,12 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
         const T S = dadd(dadd(dadd(A2, a8), a16), a24);
         if (lane < 4) sl[lane] = S;
     }
-    if constexpr (!LAD_WARP_DDOT_SMEM) W->aw[lane] = {a, wv};  // FMA tail operands as (a, w) pairs
+    if constexpr (!LAD_WARP_DDOT_SMEM) {
+        // FMA tail operands as (t - loc_i, x_ij) pairs, signed: the tail's DFMA takes |.| as operand
+        // modifiers (exact), so no separate abs instructions
+        if constexpr (LAD_WARP_RAW_AW) W->aw[lane] = {dsub(t_new, loc), (padx_v<PMAX, T> && cacheable) ? xij : wv};
+        else W->aw[lane] = {a, wv};
+    }
     __syncwarp();
     T dot = T(0);
     if (n1 > 0) {
@@ -681,7 +694,7 @@ __device__ __forceinline__ void median_update(WarpShared<PMAX, T> *W, int lane, 
     for (int t = 0; t < 16; ++t) {  // FMA tail in index order, length cnt - n1 < 16
         if (n1 + t < cnt) {
             const auto q = W->aw[n1 + t];
-            dot = dfma(q.x, q.y, dot);
+            dot = LAD_WARP_RAW_AW ? dfma(fabs(q.x), fabs(q.y), dot) : dfma(q.x, q.y, dot);
         }
     }
     __syncwarp();
@@ -806,6 +819,14 @@ __device__ LAD_WARP_DESC_ATTR void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX
     if (j >= p) {
         conv = 1;
     } else if (LAD_WARP_DENSE_LOOP && NC > 0 && sparse == 0u) {
+        uint32_t axis_list = 0u;
+        int nfree = 0;
+#pragma unroll
+        for (int jj = PMAX - 1; jj >= 0; --jj)
+            if (jj != frozen) {
+                axis_list = (axis_list << 4) | (uint32_t)(jj + 1);
+                ++nfree;
+            }
         // Every column dense (the common case): no per-step sparse test, and with
         // LAD_WARP_UNROLL the sweep over the PMAX axes is unrolled (compile-time
         // axis offsets, no axis bookkeeping); the frozen axis is skipped in place.
@@ -817,6 +838,14 @@ __device__ LAD_WARP_DESC_ATTR void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX
                     warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, jj, lam, false, r, f_cur, sum_abs_b);
                     ++steps;
                 }
+            } else if constexpr (LAD_WARP_AXIS_LIST) {
+                // the free axes in sweep order, 4 bits each (axis + 1), consumed low nibble first
+#pragma unroll 1
+                for (uint32_t lst = axis_list; lst != 0u; lst >>= 4) {
+                    const int jj = (int)(lst & 15u) - 1;
+                    warp_step<PMAX, NC, T>(W, lane, inv_mask, xrow, yrow, n, jj, lam, false, r, f_cur, sum_abs_b);
+                }
+                steps += nfree;
             } else {
 #pragma unroll 1
                 for (int jj = j0; jj < PMAX; jj += 1 + (jj + 1 == frozen)) {
