@@ -963,14 +963,19 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 // divergent: in a thread-per-problem warp some lane hits it at most steps);
 // 0 / x is the signed zero 0 * x for finite nonzero x, so a zero dividend
 // divides 1 instead and takes 0 * x.
+// Config 1, same-box A/B at B = 262,144: 9.67 M -> 11.2 M solves/s (82 -> 67 warp
+// instructions per step).  The dividend select must be opaque: otherwise the
+// compiler sees that q is unused when z and divides r itself, slow path included.
 #ifndef LAD_THREAD_ZDIV
-#define LAD_THREAD_ZDIV 0
+#define LAD_THREAD_ZDIV 1
 #endif
 __device__ __forceinline__ double div_thread(double r, double x)
 {
     if constexpr (LAD_THREAD_ZDIV) {
         const bool z = (r == 0.0);
-        const double q = ddiv(z ? 1.0 : r, x);
+        double d = z ? 1.0 : r;
+        asm("" : "+d"(d));  // opaque: the compiler would otherwise divide r itself (q is unused when z)
+        const double q = ddiv(d, x);
         return z ? dmul(r, x) : q;
     } else {
         return ddiv(r, x);
@@ -1284,7 +1289,8 @@ __host__ __device__ constexpr size_t smem_doubles_per_warp()
 // hint 8 (189) 7.18 M.  Also measured and rejected at this shape: the
 // reciprocal-table division (LAD_THREAD_RCP: more shared memory, 7.86 M), y
 // read from global memory (LAD_THREAD_YGLOBAL: 7.31 M at hint 12), a zero-
-// dividend bypass of the division's slow path (7.91 M), and the median guess
+// dividend bypass of the division's slow path written as a plain select (7.91 M:
+// the compiler undid it, see LAD_THREAD_ZDIV), and the median guess
 // (LAD_THREAD_CAND: any lane's miss makes the whole warp sort; 5.2 M vs 5.9 M).
 #ifndef LAD_THREAD_MIN_BLOCKS
 #define LAD_THREAD_MIN_BLOCKS 10

@@ -17,6 +17,12 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+import os  # noqa: E402
+
+if os.environ.get("LAD_PROF_LIB"):  # profile another build of the library (A/B captures)
+    from paper_2510_15649_b200 import _build  # noqa: E402
+
+    _build.LIB = os.path.abspath(os.environ["LAD_PROF_LIB"])
 import paper_2510_15649_b200 as lad  # noqa: E402
 from paper_2510_15649_b200 import configgen as G  # noqa: E402
 
