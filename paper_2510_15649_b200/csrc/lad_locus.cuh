@@ -972,11 +972,7 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 __device__ __forceinline__ double div_thread(double r, double x)
 {
     if constexpr (LAD_THREAD_ZDIV) {
-        const bool z = (r == 0.0);
-        double d = z ? 1.0 : r;
-        asm("" : "+d"(d));  // opaque: the compiler would otherwise divide r itself (q is unused when z)
-        const double q = ddiv(d, x);
-        return z ? dmul(r, x) : q;
+        return ddiv_zero_fast(r, x);
     } else {
         return ddiv(r, x);
     }

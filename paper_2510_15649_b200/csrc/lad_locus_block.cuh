@@ -326,7 +326,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
             const int e = tid + q * (int)blockDim.x;
             if (e < n) {
                 const double x = M.X[e * p + j];
-                M.loc[e] = dadd(ddiv(r[q], x), bj);
+                M.loc[e] = dadd(ddiv_zero_fast(r[q], x), bj);
                 M.w[e] = fabs(x);
             } else if (e == n) {
                 M.loc[e] = 0.0;

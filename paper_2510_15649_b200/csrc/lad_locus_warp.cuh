@@ -102,6 +102,12 @@ constexpr bool padx_v = LAD_WARP_PADX && fast_div_v<PMAX, T>;
 #ifndef LAD_WARP_RAW_AW
 #define LAD_WARP_RAW_AW 0
 #endif
+// IEEE division (binary64 p = 8, no reciprocal table) with zero dividends kept
+// off its slow path (ddiv_zero_fast).  Neutral here (config 4: -0.6%, same box):
+// one lane per warp meets a zero, unlike the thread kernel's 10 rows per lane.
+#ifndef LAD_WARP_ZDIV
+#define LAD_WARP_ZDIV 0
+#endif
 // Controller inlined into the warp kernel's outer loop (warp_descent stays out
 // of line).
 #ifndef LAD_WARP_INLINE_CTL
@@ -748,7 +754,7 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
         if constexpr (fast_div_v<PMAX, T>) {
             q = div_by_rcp(rr, xx, yrow[j]);  // y = 1 on pad lanes
         } else {
-            q = ddiv(rr, xx);
+            q = LAD_WARP_ZDIV ? ddiv_zero_fast(rr, xx) : ddiv(rr, xx);
         }
         const T loc = row ? dadd(q, bj) : (lane == n ? T(0) : INF);
         const T w = (padx_v<PMAX, T> || row) ? fabs(xij) : (lane == n ? lam : T(0));

@@ -53,6 +53,23 @@ __device__ __forceinline__ T div_by_rcp(T a, T b, T y)
     return q;
 }
 
+// a / b (IEEE, round to nearest) for a dividend that is often exactly zero: a
+// residual of a row that an accepted coordinate step put on its breakpoint.
+// __ddiv_rn sends a zero dividend down its full-range slow path (a call of ~60
+// instructions, and in SIMT every lane of the warp waits for it); 0 / b is the
+// signed zero 0 * b for finite nonzero b, so zero dividends divide 1 instead
+// and take 0 * b.  The dividend select is opaque to the compiler, which would
+// otherwise notice that q is unused when a == 0 and divide a itself.
+__device__ __forceinline__ double ddiv_zero_fast(double a, double b)
+{
+    const bool z = (a == 0.0);
+    double d = z ? 1.0 : a;
+    asm("" : "+d"(d));
+    const double q = __ddiv_rn(d, b);
+    return z ? __dmul_rn(a, b) : q;
+}
+__device__ __forceinline__ float ddiv_zero_fast(float a, float b) { return __fdiv_rn(a, b); }
+
 template <typename T>
 __device__ __forceinline__ T inf_of();
 template <>
