@@ -945,6 +945,11 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 #ifndef LAD_THREAD_CAND
 #define LAD_THREAD_CAND 0
 #endif
+// Thread kernel's weighted median by pairwise rank sums (step_dense) instead of
+// the sorting network; the sort stays as the exact fallback for margin cases.
+#ifndef LAD_THREAD_RANK
+#define LAD_THREAD_RANK 1
+#endif
 // Thread kernel's breakpoint division by a per-problem reciprocal table in
 // shared memory (div_by_rcp: Markstein, bit-identical to r / x), columns with
 // a divisor outside 2^+-450 on the generic path.
@@ -995,91 +1000,6 @@ __device__ __forceinline__ void bset(double (&b)[PMAX], int j, double v)
     for (int k = 0; k < PMAX; ++k) b[k] = (j == k) ? v : b[k];
 }
 
-// Dense column, compile-time n = NMAX: register sort network.
-// Returns true if the step moved beta_j.
-template <int NMAX, int PMAX>
-__device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, const double *RX,
-                                           double *Ls, int lane, int j, double lam, double &f_cur, double &sum_abs_b)
-{
-    constexpr int NE = NMAX + 1;
-    constexpr int XS = PMAX * 32;  // row stride of Xs in doubles
-    const double *xc = Xs + j * 32 + lane;
-    const double *rc = RX + j * 32 + lane;
-    const double bj = bget(b, j);
-    double key[NE];
-    int idx[NE];
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-        // np.divide then += b[j] (ccd.py:165-166)
-        double loc = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : div_thread(r[i], xc[i * XS]), bj);
-        key[i] = loc;
-        idx[i] = i;
-        Ls[i * 32 + lane] = loc;
-    }
-    key[NMAX] = 0.0;
-    idx[NMAX] = NMAX;
-    sort_pairs<NE>(key, idx);
-    auto wsorted = [&](int id) -> double {
-        int ic = id < NMAX ? id : NMAX - 1;
-        double x = xc[ic * XS];
-        return id < NMAX ? fabs(x) : lam;
-    };
-    // cum = sequential cumsum in sorted order; total = cum[-1] (ccd.py:85-86)
-    double c = 0.0;
-#pragma unroll
-    for (int k = 0; k < NE; ++k) c = dadd(c, wsorted(idx[k]));
-    const double total = c;
-    const double half = dmul(0.5, total);
-    // k = searchsorted(cum, half, 'left')
-    c = 0.0;
-    bool found = false;
-    int kk = NE;
-    double ck = 0.0, tk = key[NE - 1], tk1 = key[NE - 1];
-#pragma unroll
-    for (int k = 0; k < NE; ++k) {
-        c = dadd(c, wsorted(idx[k]));
-        bool hit = !found && (c >= half);
-        if (hit) {
-            kk = k;
-            ck = c;
-            tk = key[k];
-            tk1 = key[k + 1 < NE ? k + 1 : k];
-        }
-        found = found || hit;
-    }
-    double t_new;
-    if (kk + 1 < NE && fabs(dsub(ck, half)) <= dmul(1e-12, total)) t_new = dmul(0.5, dadd(tk, tk1));
-    else t_new = tk;
-    // skip test (ccd.py:172)
-    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
-    // v_new = lam*(sum|b| - |b_j|) + |t - locs| @ weights  (ccd.py:177-180)
-    double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
-    double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, i < NMAX ? Ls[i * 32 + lane] : 0.0)); },
-                                 [&](int i) { return i < NMAX ? fabs(xc[i * XS]) : lam; });
-    double v_new = dadd(constant, dot);
-    if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
-        double delta = dsub(t_new, bj);
-#pragma unroll
-        for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
-        sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
-        bset(b, j, t_new);
-        f_cur = v_new;
-    }
-}
-
-// Dense column, compile-time n = NMAX, with the median guessed first: the
-// element that was this axis' weighted median at its previous step (cand) is
-// usually still the median.  Element m is the reference's median iff the
-// weight ordered before it in the stable (location, index) order, Wb,
-// satisfies Wb < total/2 <= Wb + w_m in numpy's sequential cumsum
-// (ccd.py:83-88).  Wb and the total are summed here in index order, and the
-// guess is accepted only beyond a margin of 1e-9 * total on both sides: every
-// sum of NE <= 33 non-negative terms is within NE * 2^-53 * total of the
-// exact one (ours and numpy's), so an accepted guess is numpy's k, and the
-// 1e-12 * total midpoint tie (ccd.py:89-90) is excluded.  Otherwise the
-// register sort network decides as in step_dense and refreshes the guess.
-// Breakpoints stay in registers in index order for v_new (no reload); the
-// guess' location is read back through the lane's Ls column.
 constexpr double THREAD_MEDIAN_MARGIN = 1e-9;
 
 
@@ -1139,6 +1059,148 @@ __device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double
     return mp;
 }
 
+
+// Dense column, compile-time n = NMAX: register sort network.
+// Returns true if the step moved beta_j.
+template <int NMAX, int PMAX>
+__device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, const double *RX,
+                                           double *Ls, int lane, int j, double lam, double &f_cur, double &sum_abs_b)
+{
+    constexpr int NE = NMAX + 1;
+    constexpr int XS = PMAX * 32;  // row stride of Xs in doubles
+    const double *xc = Xs + j * 32 + lane;
+    const double *rc = RX + j * 32 + lane;
+    const double bj = bget(b, j);
+    double t_new;
+    if constexpr (LAD_THREAD_RANK) {
+        // Weighted median by rank sums: wb[i] = weight ordered before element i in
+        // the stable (location, index) order, one comparison per pair (for j < i, j
+        // comes first iff loc_j <= loc_i).  Sums in any order are within NE * 2^-53
+        // * total of numpy's cumsum, so element m decided beyond a 1e-9 * total
+        // margin (wb < half <= wb + w_m) is numpy's k and not the 1e-12 midpoint tie
+        // (ccd.py:83-90); otherwise (rare) the sort below decides exactly.  Every
+        // lane runs the same straight-line code: no sort, no divergence.
+        double loc[NE], w[NE], wb[NE];
+        double total = 0.0;
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) {
+            const double x = xc[i * XS];
+            // np.divide then += b[j] (ccd.py:165-166)
+            loc[i] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], x, rc[i * XS]) : div_thread(r[i], x), bj);
+            Ls[i * 32 + lane] = loc[i];
+            w[i] = fabs(x);
+            wb[i] = 0.0;
+            total = dadd(total, w[i]);
+        }
+        loc[NMAX] = 0.0;
+        w[NMAX] = lam;
+        wb[NMAX] = 0.0;
+        total = dadd(total, lam);
+#pragma unroll
+        for (int i = 1; i < NE; ++i)
+#pragma unroll
+            for (int q = 0; q < i; ++q) {
+                if (loc[q] <= loc[i]) wb[i] = dadd(wb[i], w[q]);
+                else wb[q] = dadd(wb[q], w[i]);
+            }
+        const double hlf = dmul(0.5, total), mg = dmul(THREAD_MEDIAN_MARGIN, total);
+        const double lo = dsub(hlf, mg), hi = dadd(hlf, mg);
+        bool found = false;
+        t_new = 0.0;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const bool c = (wb[i] < lo) & (dadd(wb[i], w[i]) > hi);
+            t_new = c ? loc[i] : t_new;
+            found = found | c;
+        }
+        if (!found) t_new = median_by_sort<NMAX, PMAX>(Ls, xc, lane, lam).t;
+        if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
+        const double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
+        const double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, loc[i])); }, [&](int i) { return w[i]; });
+        const double v_new = dadd(constant, dot);
+        if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
+            const double delta = dsub(t_new, bj);
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+            sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+            bset(b, j, t_new);
+            f_cur = v_new;
+        }
+        return;
+    }
+    double key[NE];
+    int idx[NE];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+        // np.divide then += b[j] (ccd.py:165-166)
+        double loc = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], xc[i * XS], rc[i * XS]) : div_thread(r[i], xc[i * XS]), bj);
+        key[i] = loc;
+        idx[i] = i;
+        Ls[i * 32 + lane] = loc;
+    }
+    key[NMAX] = 0.0;
+    idx[NMAX] = NMAX;
+    sort_pairs<NE>(key, idx);
+    auto wsorted = [&](int id) -> double {
+        int ic = id < NMAX ? id : NMAX - 1;
+        double x = xc[ic * XS];
+        return id < NMAX ? fabs(x) : lam;
+    };
+    // cum = sequential cumsum in sorted order; total = cum[-1] (ccd.py:85-86)
+    double c = 0.0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) c = dadd(c, wsorted(idx[k]));
+    const double total = c;
+    const double half = dmul(0.5, total);
+    // k = searchsorted(cum, half, 'left')
+    c = 0.0;
+    bool found = false;
+    int kk = NE;
+    double ck = 0.0, tk = key[NE - 1], tk1 = key[NE - 1];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        c = dadd(c, wsorted(idx[k]));
+        bool hit = !found && (c >= half);
+        if (hit) {
+            kk = k;
+            ck = c;
+            tk = key[k];
+            tk1 = key[k + 1 < NE ? k + 1 : k];
+        }
+        found = found || hit;
+    }
+    if (kk + 1 < NE && fabs(dsub(ck, half)) <= dmul(1e-12, total)) t_new = dmul(0.5, dadd(tk, tk1));
+    else t_new = tk;
+    // skip test (ccd.py:172)
+    if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;
+    // v_new = lam*(sum|b| - |b_j|) + |t - locs| @ weights  (ccd.py:177-180)
+    double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
+    double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, i < NMAX ? Ls[i * 32 + lane] : 0.0)); },
+                                 [&](int i) { return i < NMAX ? fabs(xc[i * XS]) : lam; });
+    double v_new = dadd(constant, dot);
+    if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
+        double delta = dsub(t_new, bj);
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+        sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+        bset(b, j, t_new);
+        f_cur = v_new;
+    }
+}
+
+// Dense column, compile-time n = NMAX, with the median guessed first: the
+// element that was this axis' weighted median at its previous step (cand) is
+// usually still the median.  Element m is the reference's median iff the
+// weight ordered before it in the stable (location, index) order, Wb,
+// satisfies Wb < total/2 <= Wb + w_m in numpy's sequential cumsum
+// (ccd.py:83-88).  Wb and the total are summed here in index order, and the
+// guess is accepted only beyond a margin of 1e-9 * total on both sides: every
+// sum of NE <= 33 non-negative terms is within NE * 2^-53 * total of the
+// exact one (ours and numpy's), so an accepted guess is numpy's k, and the
+// 1e-12 * total midpoint tie (ccd.py:89-90) is excluded.  Otherwise the
+// register sort network decides as in step_dense and refreshes the guess.
+// Breakpoints stay in registers in index order for v_new (no reload); the
+// guess' location is read back through the lane's Ls column.
 template <int NMAX, int PMAX>
 __device__ __forceinline__ void step_dense_cand(double (&r)[NMAX], double (&b)[PMAX], int (&cand)[PMAX],
                                                 const double *Xs, const double *RX, double *Ls, const double *Tw,
