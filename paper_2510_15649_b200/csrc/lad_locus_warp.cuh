@@ -40,12 +40,16 @@ constexpr unsigned FULLMASK = 0xffffffffu;
 #ifndef LAD_WARP_WARPS_WIDE
 #define LAD_WARP_WARPS_WIDE 7
 #endif
+#ifndef LAD_WARP_F32_WIDE  // binary32 p = 8 with the binary64 p = 8 shape (7 warps, 72 registers)
+#define LAD_WARP_F32_WIDE 0
+#endif
 #ifndef LAD_WARP_MIN_BLOCKS
 #define LAD_WARP_MIN_BLOCKS 4
 #endif
 constexpr int WARP_MIN_BLOCKS = LAD_WARP_MIN_BLOCKS;
 template <int PMAX, typename T>
-constexpr int warps_per_block = (PMAX <= 5 || sizeof(T) == 4) ? LAD_WARP_WARPS_NARROW : LAD_WARP_WARPS_WIDE;
+constexpr int warps_per_block = (PMAX <= 5 || (sizeof(T) == 4 && !LAD_WARP_F32_WIDE)) ? LAD_WARP_WARPS_NARROW
+                                                                                    : LAD_WARP_WARPS_WIDE;
 
 // Division by a precomputed reciprocal: q = RN(r * y), then two corrections
 // q += RN(r - q * x) * y with y = RN(1 / x).  The first makes q faithful, the
@@ -788,16 +792,22 @@ __device__ __forceinline__ T warp_objective(WarpShared<PMAX, T> *W, int lane, in
 }
 
 // ccd_descend (ccd.py:126-206) for the descent request in C, all lanes.
+// The descent and the controller are inlined into the kernel (binary64: +1.6%
+// and +2.1% for config 2).  The binary32 p = 8 kernel spills ~690 B per thread
+// at its 64-register cap when inlined and is still fastest that way (config 4
+// fp32, same box: 157 k inlined, 149 k out of line (no spills), 148 k / 146 k
+// with 7 warps at 72 registers (LAD_WARP_F32_WIDE) inlined / out of line).
 #ifndef LAD_WARP_INLINE_DESC
 #define LAD_WARP_INLINE_DESC 1
 #endif
-#if LAD_WARP_INLINE_DESC
-#define LAD_WARP_DESC_ATTR __forceinline__
-#else
-#define LAD_WARP_DESC_ATTR __noinline__
+#ifndef LAD_WARP_F32_INLINE
+#define LAD_WARP_F32_INLINE 1
 #endif
+template <typename T>
+constexpr bool warp_inline_v = sizeof(T) == 8 || LAD_WARP_F32_INLINE;
+
 template <int PMAX, int NC, typename T>
-__device__ LAD_WARP_DESC_ATTR void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
+__device__ __forceinline__ void warp_descent_body(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
                                           int p_rt)
 {
     const int n = NC > 0 ? NC : n_rt;
@@ -907,6 +917,13 @@ __device__ LAD_WARP_DESC_ATTR void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX
     __syncwarp();
 }
 
+template <int PMAX, int NC, typename T>
+__device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, int lane, uint32_t inv_mask, int n_rt,
+                                          int p_rt)
+{
+    warp_descent_body<PMAX, NC, T>(W, C, lane, inv_mask, n_rt, p_rt);
+}
+
 // PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
 template <int PMAX, int NC, typename T>
 __global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
@@ -927,10 +944,14 @@ __global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS
     for (;;) {
         // inlined: the controller reads LocusArgs straight from the kernel's parameter
         // (constant) bank; out of line it reads every field from a per-lane stack copy
-        int act = LAD_WARP_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot) : controller<PMAX>(C, A, acc, slot);
+        int act = (LAD_WARP_INLINE_CTL && warp_inline_v<T>) ? controller_body<PMAX>(C, A, acc, slot)
+                                                            : controller<PMAX>(C, A, acc, slot);
         __syncwarp();
         if (act == ACT_EXIT) break;
-        warp_descent<PMAX, NC, T>(W, C, lane, inv_mask, n, p);
+        if constexpr (LAD_WARP_INLINE_DESC && warp_inline_v<T>)
+            warp_descent_body<PMAX, NC, T>(W, C, lane, inv_mask, n, p);
+        else
+            warp_descent<PMAX, NC, T>(W, C, lane, inv_mask, n, p);
     }
 }
 
