@@ -1350,8 +1350,10 @@ __host__ __device__ constexpr size_t smem_doubles_per_warp()
 // dividend bypass of the division's slow path written as a plain select (7.91 M:
 // the compiler undid it, see LAD_THREAD_ZDIV), and the median guess
 // (LAD_THREAD_CAND: any lane's miss makes the whole warp sort; 5.2 M vs 5.9 M).
+// Re-swept after the direct-jump controller, the zero-dividend division and the rank-sum
+// median (B = 262,144): hints 8 / 10 / 12 / 14 / 16 -> 11.08 / 11.75 / 12.00 / 11.37 / 11.37 M.
 #ifndef LAD_THREAD_MIN_BLOCKS
-#define LAD_THREAD_MIN_BLOCKS 10
+#define LAD_THREAD_MIN_BLOCKS 12
 #endif
 template <int NMAX, bool EXACT>
 constexpr int thread_min_blocks = (EXACT && NMAX <= 10) ? LAD_THREAD_MIN_BLOCKS : 1;
