@@ -195,14 +195,24 @@ __device__ double objective_of(const double *Xs, const double *Yp, int ys, int n
     return dadd(rs, dmul(lam, bs));
 }
 
-#define ISSUE(START_EXPR, FROZEN, TOL, SWEEPS, NEXT)                    \
-    do {                                                                \
-        for (int jj_ = 0; jj_ < p; ++jj_) C.req_start[jj_] = (START_EXPR); \
-        C.req_frozen = (FROZEN);                                        \
-        C.req_tol = (TOL);                                              \
-        C.req_sweeps = (SWEEPS);                                        \
-        C.pc = (NEXT);                                                  \
-        return ACT_DESCENT;                                             \
+// The start vector is written through acc.lanes (one element per lane in the
+// warp kernel); ISSUE_SEQ writes it sequentially, for starts held in a
+// per-thread array (a lane-indexed read of it would go through local memory).
+#define ISSUE_TAIL(FROZEN, TOL, SWEEPS, NEXT) \
+    C.req_frozen = (FROZEN);                 \
+    C.req_tol = (TOL);                       \
+    C.req_sweeps = (SWEEPS);                 \
+    C.pc = (NEXT);                           \
+    return ACT_DESCENT;
+#define ISSUE(START_EXPR, FROZEN, TOL, SWEEPS, NEXT)                              \
+    do {                                                                          \
+        acc.lanes(p, [&](int jj_) { C.req_start[jj_] = (START_EXPR); });          \
+        ISSUE_TAIL(FROZEN, TOL, SWEEPS, NEXT)                                     \
+    } while (0)
+#define ISSUE_SEQ(START_EXPR, FROZEN, TOL, SWEEPS, NEXT)                          \
+    do {                                                                          \
+        for (int jj_ = 0; jj_ < p; ++jj_) C.req_start[jj_] = (START_EXPR);        \
+        ISSUE_TAIL(FROZEN, TOL, SWEEPS, NEXT)                                     \
     } while (0)
 
 #define PROBE(T, RET)            \
@@ -212,18 +222,18 @@ __device__ double objective_of(const double *Xs, const double *Yp, int ys, int n
         goto L_PC_PR_BEGIN;      \
     } while (0)
 
-template <int PMAX>
-__device__ __forceinline__ void set_point_from_result(Ctl<PMAX> &C, Point<PMAX> &P, double t, int p)
+template <int PMAX, class AC>
+__device__ __forceinline__ void set_point_from_result(const AC &acc, Ctl<PMAX> &C, Point<PMAX> &P, double t, int p)
 {
     P.t = t;
-    for (int j = 0; j < p; ++j) P.beta[j] = C.res_beta[j];
     P.value = C.res_obj;
     P.conv = C.res_conv;
+    acc.lanes(p, [&](int j) { P.beta[j] = C.res_beta[j]; });
 }
 
-template <int PMAX>
-__device__ __forceinline__ void seen_append(const LocusArgs &A, double *seen, Ctl<PMAX> &C, const Point<PMAX> &P,
-                                            int p, bool leader)
+template <int PMAX, class AC>
+__device__ __forceinline__ void seen_append(const AC &acc, const LocusArgs &A, double *seen, Ctl<PMAX> &C,
+                                            const Point<PMAX> &P, int p)
 {
     if (seen == nullptr) return;
     int k = C.nseen;
@@ -231,11 +241,11 @@ __device__ __forceinline__ void seen_append(const LocusArgs &A, double *seen, Ct
         C.seen_over = 1;    // problem ends with status 3 instead of a silently different warm start
         return;
     }
-    if (leader) {
-        seen[k] = P.t;
-        double *sb = seen + A.seen_cap + (size_t)k * PMAX;
-        for (int j = 0; j < p; ++j) sb[j] = P.beta[j];
-    }
+    double *sb = seen + A.seen_cap + (size_t)k * PMAX;
+    acc.lanes_out(1 + p, [&](int q) {
+        if (q == 0) seen[k] = P.t;
+        else sb[q - 1] = P.beta[q - 1];
+    });
     C.nseen = k + 1;
 }
 
@@ -326,6 +336,28 @@ struct ThreadAccess {
     double *RX;  // RN(1 / x_ij), same layout as Xs (division by reciprocal), or null
     __device__ __forceinline__ bool leader() const { return true; }
     __device__ __forceinline__ void sync() const {}
+    // this slot's curve-point scratch (seen list), null when unused (p <= 2)
+    template <int PM>
+    __device__ __forceinline__ double *seen_base(const LocusArgs &A, int slot) const
+    {
+        return (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PM) : nullptr;
+    }
+    // element-wise work on controller vectors: f(k) for k < cnt (Ctl fields / outputs)
+    template <class F>
+    __device__ __forceinline__ void lanes(int cnt, F f) const
+    {
+        for (int k = 0; k < cnt; ++k) f(k);
+    }
+    template <class F>
+    __device__ __forceinline__ void lanes_out(int cnt, F f) const
+    {
+        for (int k = 0; k < cnt; ++k) f(k);
+    }
+    template <int PM>
+    __device__ __forceinline__ void copy_point(Point<PM> &d, const Point<PM> &s) const
+    {
+        d = s;
+    }
     // count one finished unit on *ctr; true for the caller that completes `of` units
     __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
     {
@@ -415,7 +447,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
 {
     const int n = acc.n;
     const int p = acc.p;
-    double *seen = (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PMAX) : nullptr;
+    double *seen = acc.template seen_base<PMAX>(A, slot);
     for (;;) {
         acc.sync();
         switch (C.pc) {
@@ -681,11 +713,11 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             double agree = dmul(p > 3 ? 1e-6 : 1e-7, C.a_idx == 0 ? 1.0 : fmax(1.0, fabs(C.best.value)));
             bool brk = false;
             if (C.a_idx == 0) {
-                C.best = ab;
+                acc.copy_point(C.best, ab);
                 C.best_axis = C.axis;
                 C.confirmations = 1;
             } else if (ab.value < dsub(C.best.value, agree)) {
-                C.best = ab;
+                acc.copy_point(C.best, ab);
                 C.best_axis = C.axis;
                 C.confirmations = 1;
             } else if (fabs(dsub(ab.value, C.best.value)) <= agree) {
@@ -731,11 +763,11 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
         case PC_REF_AXIS_START: {
             int axis = C.refine_axes[C.q];
             evaluator_reset(C, axis, A, p);
-            C.seeded = C.best;
+            acc.copy_point(C.seeded, C.best);
             C.seeded.t = C.best.beta[axis];
             C.seeded.conv = 1;
-            seen_append(A, seen, C, C.seeded, p, acc.leader());
-            C.ev_best = C.seeded;
+            seen_append(acc, A, seen, C, C.seeded, p);
+            acc.copy_point(C.ev_best, C.seeded);
             C.has_best = 1;
             C.margin = dmul(C.margin_scale, fmax(1.0, fabs(C.seeded.value)));
             C.rng.seed(0x5EEDULL + (uint64_t)axis, 54);
@@ -754,14 +786,14 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                     st[j] = dadd(st[j], dmul(du, fmax(1.0, fabs(C.seeded.beta[j]))));
                 }
                 st[C.axis] = C.seeded.t;
-                ISSUE(st[jj_], C.axis, C.fast_tol, C.fast_sweeps, PC_REF_FAN_AFTER);
+                ISSUE_SEQ(st[jj_], C.axis, C.fast_tol, C.fast_sweeps, PC_REF_FAN_AFTER);
             }
             C.w = C.width;
             C.rr = 0;
             goto L_PC_REF_ROUND;
         }
         case PC_REF_FAN_AFTER: {
-            set_point_from_result(C, C.pt, C.seeded.t, p);
+            set_point_from_result(acc, C, C.pt, C.seeded.t, p);
             if (C.pt.value <= dadd(C.ev_best.value, C.margin)) {
                 double tt = C.seeded.t;
                 ISSUE(jj_ == C.axis ? tt : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_REF_FAN_REFINED);
@@ -769,14 +801,14 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             goto L_PC_REF_FAN_FINISH;
         }
         case PC_REF_FAN_REFINED: {
-            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.seeded.t, p);
+            if (C.res_obj < C.pt.value) set_point_from_result(acc, C, C.pt, C.seeded.t, p);
             goto L_PC_REF_FAN_FINISH;
         }
         L_PC_REF_FAN_FINISH:
         case PC_REF_FAN_FINISH: {
             C.ev_calls++;
-            seen_append(A, seen, C, C.pt, p, acc.leader());
-            if (C.pt.value < C.ev_best.value) C.ev_best = C.pt;
+            seen_append(acc, A, seen, C, C.pt, p);
+            if (C.pt.value < C.ev_best.value) acc.copy_point(C.ev_best, C.pt);
             C.fan_i++;
             goto L_PC_REF_FAN;
         }
@@ -813,7 +845,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             C.calls += C.ev_calls;
             C.failures += C.ev_failures;
             if (cand.value < dsub(C.best.value, dmul(1e-9, fmax(1.0, fabs(C.best.value))))) C.improved = 1;
-            if (cand.value < C.best.value) C.best = cand;
+            if (cand.value < C.best.value) acc.copy_point(C.best, cand);
             C.q++;
             if (C.q < C.nref) {
                 goto L_PC_REF_AXIS_START;
@@ -869,7 +901,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             ISSUE(jj_ == C.axis ? t : 0.0, C.axis, C.fast_tol, C.fast_sweeps, PC_PR_AFTER_COLD);
         }
         case PC_PR_AFTER_COLD: {
-            set_point_from_result(C, C.pt, C.probe_t, p);
+            set_point_from_result(acc, C, C.pt, C.probe_t, p);
             if (C.warm_idx >= 0 && p > 2) {
                 const double *wb = seen + A.seen_cap + (size_t)C.warm_idx * PMAX;
                 double t = C.probe_t;
@@ -878,11 +910,11 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             goto L_PC_PR_REFINE_CHECK;
         }
         case PC_PR_AFTER_WARM: {
-            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
+            if (C.res_obj < C.pt.value) set_point_from_result(acc, C, C.pt, C.probe_t, p);
             goto L_PC_PR_REFINE_CHECK;
         }
         case PC_PR_AFTER_FAST_ONLY: {
-            set_point_from_result(C, C.pt, C.probe_t, p);
+            set_point_from_result(acc, C, C.pt, C.probe_t, p);
             goto L_PC_PR_REFINE_CHECK;
         }
         L_PC_PR_REFINE_CHECK:
@@ -896,14 +928,14 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             goto L_PC_PR_FINISH;
         }
         case PC_PR_AFTER_REFINE: {
-            if (C.res_obj < C.pt.value) set_point_from_result(C, C.pt, C.probe_t, p);
+            if (C.res_obj < C.pt.value) set_point_from_result(acc, C, C.pt, C.probe_t, p);
             goto L_PC_PR_FINISH;
         }
         L_PC_PR_FINISH:
         case PC_PR_FINISH: {
             C.ev_calls++;
             C.ev_failures += C.pt.conv ? 0 : 1;
-            seen_append(A, seen, C, C.pt, p, acc.leader());
+            seen_append(acc, A, seen, C, C.pt, p);
             if (!C.has_best || C.pt.value < C.ev_best.value) {
                 C.ev_best = C.pt;
                 C.has_best = 1;

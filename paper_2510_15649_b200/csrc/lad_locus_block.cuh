@@ -131,6 +131,29 @@ struct BlockAccess {
     BlockMem<PMAX> M;
     __device__ __forceinline__ bool leader() const { return threadIdx.x == 0; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
+    template <int PM>
+    __device__ __forceinline__ double *seen_base(const LocusArgs &A, int slot) const
+    {
+        return (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PM) : nullptr;
+    }
+    // controller vectors: every thread writes the same shared values (lanes), the
+    // leader alone writes global outputs (lanes_out)
+    template <class F>
+    __device__ __forceinline__ void lanes(int cnt, F f) const
+    {
+        for (int k = 0; k < cnt; ++k) f(k);
+    }
+    template <class F>
+    __device__ __forceinline__ void lanes_out(int cnt, F f) const
+    {
+        if (threadIdx.x == 0)
+            for (int k = 0; k < cnt; ++k) f(k);
+    }
+    template <int PM>
+    __device__ __forceinline__ void copy_point(Point<PM> &d, const Point<PM> &s) const
+    {
+        d = s;
+    }
     __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
     {
         __syncthreads();

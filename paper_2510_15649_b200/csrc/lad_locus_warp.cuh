@@ -117,6 +117,16 @@ constexpr bool padx_v = LAD_WARP_PADX && fast_div_v<PMAX, T>;
 #ifndef LAD_WARP_INLINE_CTL
 #define LAD_WARP_INLINE_CTL 1
 #endif
+// The nearest-seen-point argmin (locus.py:188-191) by REDUX minima on the
+// distance's bit pattern and the index instead of a five-round shuffle tree.
+#ifndef LAD_WARP_NEAREST_REDUX
+#define LAD_WARP_NEAREST_REDUX 1
+#endif
+// Controller vectors (descent start, result beta, curve points) copied one
+// element per lane (WarpAccess::lanes) instead of by every lane in turn.
+#ifndef LAD_WARP_CTL_LANES
+#define LAD_WARP_CTL_LANES 1
+#endif
 // The median test's half-total weight by a broadcast load (1 instruction)
 // instead of a REDUX into a uniform register.
 #ifndef LAD_WARP_HQ_LDS
@@ -138,6 +148,7 @@ struct WarpShared {
     unsigned wq[PMAX][32];  // per axis: weights in fixed point, floor(w_i * 2^30 / total)
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
     uint2 hqb[PMAX];        // per axis: (halfq - margin (0 if below), halfq + margin)
+    double *seen;           // this slot's seen-list scratch (null when unused), set at kernel start
     alignas(16) T pp[32];   // ddot lane-tree products, lane l's four at [4 l, 4 l + 4) (n1 = 16) / [8 l, 8 l + 8)
 };
 
@@ -255,6 +266,49 @@ struct WarpAccess {
     WarpShared<PMAX, T> *W;
     __device__ __forceinline__ bool leader() const { return lane == 0; }
     __device__ __forceinline__ void sync() const { __syncwarp(); }
+    // the slot's seen list, computed once per kernel (WarpShared::seen)
+    template <int PM>
+    __device__ __forceinline__ double *seen_base(const LocusArgs &, int) const
+    {
+        return W->seen;
+    }
+    // Controller vectors one element per lane (LAD_WARP_CTL_LANES) instead of
+    // every lane repeating the whole loop on the shared Ctl; the warp syncs
+    // around the writes (the other lanes read them next).
+    template <class F>
+    __device__ __forceinline__ void lanes(int cnt, F f) const
+    {
+        if constexpr (LAD_WARP_CTL_LANES) {
+            __syncwarp();
+            if (lane < cnt) f(lane);
+            __syncwarp();
+        } else {
+            for (int k = 0; k < cnt; ++k) f(k);
+        }
+    }
+    template <class F>
+    __device__ __forceinline__ void lanes_out(int cnt, F f) const
+    {
+        if constexpr (LAD_WARP_CTL_LANES) {
+            if (lane < cnt) f(lane);
+        } else if (lane == 0) {
+            for (int k = 0; k < cnt; ++k) f(k);
+        }
+    }
+    template <int PM>
+    __device__ __forceinline__ void copy_point(Point<PM> &d, const Point<PM> &s) const
+    {
+        if constexpr (LAD_WARP_CTL_LANES) {
+            static_assert(sizeof(Point<PM>) % 8 == 0, "Point is copied in 8-byte words");
+            constexpr int nw = sizeof(Point<PM>) / 8;
+            __syncwarp();
+            if (lane < nw) reinterpret_cast<unsigned long long *>(&d)[lane] =
+                               reinterpret_cast<const unsigned long long *>(&s)[lane];
+            __syncwarp();
+        } else {
+            d = s;
+        }
+    }
     // count one finished unit on *ctr (lane 0, after the warp's global writes are
     // fenced); true in every lane for the warp that completes `of` units
     __device__ __forceinline__ bool last_of(unsigned *ctr, unsigned of) const
@@ -382,16 +436,31 @@ struct WarpAccess {
                 bk = k;
             }
         }
+        if constexpr (LAD_WARP_NEAREST_REDUX) {
+            // (distance, k) lexicographic minimum by three REDUX.MIN: a distance
+            // is >= 0, so its bit pattern orders like its value (high word, then
+            // low word), and among equal distances the lowest k wins (the
+            // reference's first minimum).  Lanes without an entry hold (inf, INT_MAX).
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(bd);
+            const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+            const unsigned mh = __reduce_min_sync(FULLMASK, hi);
+            const bool c1 = hi == mh;
+            const unsigned ml = __reduce_min_sync(FULLMASK, c1 ? lo : ~0u);
+            const bool c2 = c1 && lo == ml;
+            const unsigned mk = __reduce_min_sync(FULLMASK, c2 ? (unsigned)bk : ~0u);
+            return mk >= 0x7fffffffu ? -1 : (int)mk;
+        } else {
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            double od = shfl_xor_t(bd, off);
-            int ok = __shfl_xor_sync(FULLMASK, bk, off);
-            if (od < bd || (od == bd && ok < bk)) {
-                bd = od;
-                bk = ok;
+            for (int off = 16; off > 0; off >>= 1) {
+                double od = shfl_xor_t(bd, off);
+                int ok = __shfl_xor_sync(FULLMASK, bk, off);
+                if (od < bd || (od == bd && ok < bk)) {
+                    bd = od;
+                    bk = ok;
+                }
             }
+            return bk == 0x7fffffff ? -1 : bk;
         }
-        return bk == 0x7fffffff ? -1 : bk;
     }
 };
 
@@ -939,7 +1008,10 @@ __global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS
     const uint32_t inv_mask = bitonic_inv_mask(lane);
     Ctl<PMAX> &C = W->C;
     if (lane < PMAX) W->cand[lane] = 0;
-    if (lane == 0) C.pc = PC_FETCH;
+    if (lane == 0) {
+        C.pc = PC_FETCH;
+        W->seen = (A.seen != nullptr && p > 2) ? A.seen + (size_t)slot * A.seen_cap * (1 + PMAX) : nullptr;
+    }
     __syncwarp();
     for (;;) {
         // inlined: the controller reads LocusArgs straight from the kernel's parameter

@@ -13,7 +13,7 @@ for w in $works; do
 import csv,sys; r=list(csv.reader(sys.stdin)); h=r[0]; print(r[-1][h.index('Kernel Name')])")
   units=$(python -c "import json;print(json.load(open('gpurun_out/prof/units_$w.json')).get('units',1))")
   if [ -n "$mangled" ]; then
-    python scripts/ncu_lines.py $rep paper_2510_15649_b200/libladlasso_b200.so $mangled --top 80 --sass-top 120 --per $units \
+    python scripts/ncu_lines.py $rep paper_2510_15649_b200/libladlasso_b200.so $mangled --top ${LINES_TOP:-80} --sass-top 120 --per $units \
       > gpurun_out/prof/lines_$w.txt 2>&1
   fi
   sz=$(stat -c %s $rep)
