@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
     ap.add_argument("--solver", choices=["locus", "lp", "brute"], default="locus",
                     help="locus (the metric); lp = the simplex on config-2 problems; brute = the check on config 1")
+    ap.add_argument("--warm-groups", type=int, default=4,
+                    help="--warm: dataset groups walking their lambda stages on concurrent streams (path.py)")
     ap.add_argument("--warm", action="store_true",
                     help="config 2 warm-start lambda path (previous lambda's solution seeds the bracket)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
@@ -212,7 +214,7 @@ def workload_config(config, a, world):
         cfg["warm"] = True
         cfg["description"] += ("; warm-started path: largest lambda first, then initial_bracket (-R, R), "
                                "R = max(1, 2 max|beta_prev|) (paper_2510_15649_b200/path.py), 16 dependent "
-                               "launches per variant")
+                               f"stages per variant, {a.warm_groups} dataset groups on concurrent streams")
     return cfg
 
 
@@ -585,7 +587,7 @@ def main():
     def solve(s):
         X, Y, L = wl.inputs(s)
         if a.warm:  # 16 dependent launches per variant (path.py: largest lambda first, bracketed)
-            return [flat(lad.solve_lambda_path_batched(X, Y, LAMBDA_GRID, c, warm=True)) for c in cfgs]
+            return [flat(lad.solve_lambda_path_batched(X, Y, LAMBDA_GRID, c, warm=True, groups=a.warm_groups)) for c in cfgs]
         return [lad.solve_locus_batched(X, Y, L, c, data_index=wl.data_index) for c in cfgs]
 
     for s in range(a.warmup):
@@ -642,7 +644,7 @@ def main():
     # untimed warm-up of the host-buffer path at full size (the device memory pool grows to the
     # step's buffers once; the device-side arm likewise runs its warm-up steps untimed)
     if a.warm:
-        lad.solve_lambda_path_batched(host[0][0], host[0][1], LAMBDA_GRID, cfgs[0], warm=True)
+        lad.solve_lambda_path_batched(host[0][0], host[0][1], LAMBDA_GRID, cfgs[0], warm=True, groups=a.warm_groups)
     else:
         lad.solve_locus_batched(host[0][0], host[0][1], host[0][2], cfgs[0], data_index=hidx_np)
     barrier()
@@ -650,8 +652,8 @@ def main():
     for k in range(e2e_steps):
         h = host[k % n_host]
         for c in cfgs:  # each variant is one public-API call with its own H2D and D2H
-            if a.warm:  # one host-buffer call per lambda stage (inputs and results cross each time)
-                lad.solve_lambda_path_batched(h[0], h[1], LAMBDA_GRID, c, warm=True)
+            if a.warm:  # one public-API call per variant: X and Y cross once, every stage's results come back
+                lad.solve_lambda_path_batched(h[0], h[1], LAMBDA_GRID, c, warm=True, groups=a.warm_groups)
             else:
                 lad.solve_locus_batched(h[0], h[1], h[2], c, data_index=hidx_np)
     barrier()
@@ -662,9 +664,8 @@ def main():
     e2e_value = world * e2e_steps * solves_per_step / float(te.item())
     h2d = len(cfgs) * (sum(x.nbytes for x in host[0]) + (hidx_np.nbytes if hidx_np is not None else 0))
     d2h = solves_per_step * (wl.p * 8 + 8 + 4 + 4 + 1 + 1 + 4 + 8)
-    if a.warm:  # per variant: 16 stages x (X, Y, lambda and bracket per dataset)
-        nd = host[0][0].shape[0]
-        h2d = len(cfgs) * 16 * (host[0][0].nbytes + host[0][1].nbytes + nd * 8 + nd * 16)
+    if a.warm:  # per variant: X and Y once (lambdas and brackets are made on the device)
+        h2d = len(cfgs) * (host[0][0].nbytes + host[0][1].nbytes)
 
     # DRAM traffic per launch and warp instructions per coordinate step from the committed
     # ncu --set full capture of this workload (None otherwise)

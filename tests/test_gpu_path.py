@@ -44,6 +44,37 @@ def test_warm_path_matches_oracle_replay_at_scale(oracle):
         assert np.array_equal(r["steps"].cpu().numpy(), o["steps"])
 
 
+@pytest.mark.parametrize("on_device", [True, False])
+def test_warm_path_stream_groups_equal_one_group(monkeypatch, on_device):
+    """Dataset groups walking their stages on concurrent streams (path.py) give the single-stream
+    result, bit for bit, for device tensors and for host arrays (one upload, one download)."""
+    from paper_2510_15649_b200 import path
+
+    X, Y, _ = G.generate(2, 96, seed=15651, first=777)
+    lams = G.LAMBDA_GRID[::3]
+    cfg = lad.LocusConfig(outer_search="quadrature")
+    one = lad.solve_lambda_path_batched(X, Y, lams, cfg, warm=True, groups=1)
+    monkeypatch.setattr(path, "MIN_GROUP", 16)
+    args = (X, Y) if on_device else (X.cpu().numpy(), Y.cpu().numpy())
+    for groups in (2, 5):
+        r = lad.solve_lambda_path_batched(*args, lams, cfg, warm=True, groups=groups)
+        for f in path.FIELDS:
+            got = r[f].cpu().numpy() if on_device else np.asarray(r[f])
+            assert got.shape == tuple(one[f].shape)
+            assert np.array_equal(got, one[f].cpu().numpy()), f
+
+
+def test_warm_path_large_max_iterations_keeps_bounded_scratch():
+    """outer_max_iterations large enough that the worst-case scratch is not used: the per-stage
+    status-3 inspection path gives the same results as the default."""
+    X, Y, _ = G.generate(2, 24, seed=15651, first=99)
+    lams = G.LAMBDA_GRID[::5]
+    ref = lad.solve_lambda_path_batched(X, Y, lams, lad.LocusConfig(), warm=True)
+    r = lad.solve_lambda_path_batched(X, Y, lams, lad.LocusConfig(outer_max_iterations=5000), warm=True)
+    assert torch.equal(r["objective"], ref["objective"])
+    assert torch.equal(r["beta"], ref["beta"])
+
+
 def test_cold_path_equals_independent_solves():
     X, Y, _ = G.generate(2, 64, seed=15651)
     lams = G.LAMBDA_GRID
