@@ -453,6 +453,10 @@ def run_aux(a, world, rank, local):
     launches0 = _lib.kernel_launches()
     with ClockSampler(local) as clk:
         barrier()
+        # a step here is a few ms of GPU time, about what the host needs to enqueue it: a short spin
+        # kernel first lets the host run ahead, so the events time the GPU and not the enqueue gaps
+        if hasattr(torch.cuda, "_sleep"):
+            torch.cuda._sleep(200_000_000)
         for k in range(a.steps):
             flush.zero_()
             evs[k][0].record(stream)
