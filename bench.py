@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--block4", type=int, default=1 << 16, help="config 4 problems per step per GPU")
     ap.add_argument("--solver", choices=["locus", "lp", "brute"], default="locus",
                     help="locus (the metric); lp = the simplex on config-2 problems; brute = the check on config 1")
-    ap.add_argument("--warm-groups", type=int, default=4,
+    ap.add_argument("--warm-groups", type=int, default=2,
                     help="--warm: dataset groups walking their lambda stages on concurrent streams (path.py)")
     ap.add_argument("--warm", action="store_true",
                     help="config 2 warm-start lambda path (previous lambda's solution seeds the bracket)")

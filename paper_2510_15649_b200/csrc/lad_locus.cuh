@@ -112,7 +112,10 @@ enum : int {
 // problem's last axis search finishes the problem (PC_AXIS_COUNT)
 enum : int { AXIS_SERIAL = 0, AXIS_SEARCH = 1 };
 
-enum : int { ACT_DESCENT = 0, ACT_EXIT = 1 };
+// ACT_YIELD (thread kernel, LAD_THREAD_YIELD): the controller stopped at a state every lane passes
+// through (the curve evaluator's begin / finish); the caller re-enters it once all lanes of the warp
+// that are in the controller have yielded or finished, so those states run converged.
+enum : int { ACT_DESCENT = 0, ACT_EXIT = 1, ACT_YIELD = 2 };
 
 template <int PMAX>
 struct Ctl {
@@ -215,11 +218,25 @@ __device__ double objective_of(const double *Xs, const double *Yp, int ys, int n
         ISSUE_TAIL(FROZEN, TOL, SWEEPS, NEXT)                                     \
     } while (0)
 
-#define PROBE(T, RET)            \
-    do {                         \
-        C.probe_t = (T);         \
-        C.ret_pc = (RET);        \
-        goto L_PC_PR_BEGIN;      \
+#define PROBE(T, RET)                  \
+    do {                               \
+        C.probe_t = (T);               \
+        C.ret_pc = (RET);              \
+        if constexpr (AC::kYield) {    \
+            C.pc = PC_PR_BEGIN;        \
+            return ACT_YIELD;          \
+        } else {                       \
+            goto L_PC_PR_BEGIN;        \
+        }                              \
+    } while (0)
+#define PROBE_FINISH()                 \
+    do {                               \
+        if constexpr (AC::kYield) {    \
+            C.pc = PC_PR_FINISH;       \
+            return ACT_YIELD;          \
+        } else {                       \
+            goto L_PC_PR_FINISH;       \
+        }                              \
     } while (0)
 
 template <int PMAX, class AC>
@@ -328,8 +345,15 @@ __device__ __forceinline__ int nearest_serial(const double *seen, int lim, doubl
 
 // Access policy of the thread-per-problem kernel: the lane owns its problem;
 // data lives in the lane's column of the interleaved shared arrays.
+// Thread kernel: the controller yields at the curve evaluator's begin / finish states and is
+// re-entered with the warp's controller lanes converged (ACT_YIELD), so those states, which every
+// lane passes through on its own path, execute once per round instead of once per diverged group.
+#ifndef LAD_THREAD_YIELD
+#define LAD_THREAD_YIELD 1
+#endif
 template <int NMAX, int PMAX>
 struct ThreadAccess {
+    static constexpr bool kYield = LAD_THREAD_YIELD != 0;
     int n, p, lane;
     double *Xs, *Ys;
     double *Tw;  // per axis: sum of the breakpoint weights (|x_ij| and lambda), any order (median guess test)
@@ -925,11 +949,11 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                 double t = C.probe_t;
                 ISSUE(jj_ == C.axis ? t : C.pt.beta[jj_], C.axis, C.inner_tol, C.inner_sweeps, PC_PR_AFTER_REFINE);
             }
-            goto L_PC_PR_FINISH;
+            PROBE_FINISH();
         }
         case PC_PR_AFTER_REFINE: {
             if (C.res_obj < C.pt.value) set_point_from_result(acc, C, C.pt, C.probe_t, p);
-            goto L_PC_PR_FINISH;
+            PROBE_FINISH();
         }
         L_PC_PR_FINISH:
         case PC_PR_FINISH: {
@@ -942,6 +966,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             C.probe_v = C.pt.value;
             C.pc = C.ret_pc;  // the probe's caller: the one dynamic transition (through the switch)
+            if constexpr (AC::kYield) return ACT_YIELD;
             break;
         }
         default:
@@ -952,6 +977,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
 
 #undef ISSUE
 #undef PROBE
+#undef PROBE_FINISH
 
 // Out-of-line controller (the warp kernels: a cold path next to the step loop).
 template <int PMAX, class AC>
@@ -1432,10 +1458,24 @@ __global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kern
     for (;;) {
         __syncwarp();
         if (!__any_sync(0xffffffffu, alive)) break;
+        const unsigned ctl_lanes = __ballot_sync(0xffffffffu, alive && need_ctl);
         if (alive && need_ctl) {
             ThreadAccess<NMAX, PMAX> acc{n, p, lane, Xs, Ys, EXACT && LAD_THREAD_CAND ? Tw : nullptr,
                                          EXACT && LAD_THREAD_RCP ? RX : nullptr};
-            int act = LAD_THREAD_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot) : controller<PMAX>(C, A, acc, slot);
+            int act;
+            if constexpr (ThreadAccess<NMAX, PMAX>::kYield) {
+                // rounds: every lane still in the controller runs to its next yield point, request or
+                // exit; the vote brings the lanes back together before the next round
+                act = ACT_YIELD;
+                for (;;) {
+                    if (act == ACT_YIELD)
+                        act = LAD_THREAD_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot)
+                                                    : controller<PMAX>(C, A, acc, slot);
+                    if (!__any_sync(ctl_lanes, act == ACT_YIELD)) break;
+                }
+            } else {
+                act = LAD_THREAD_INLINE_CTL ? controller_body<PMAX>(C, A, acc, slot) : controller<PMAX>(C, A, acc, slot);
+            }
             if (act == ACT_EXIT) {
                 alive = false;
             } else {

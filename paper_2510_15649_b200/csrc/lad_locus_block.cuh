@@ -127,6 +127,7 @@ __device__ __forceinline__ double block_sum_d(double v, double *red)
 // Access policy of the block kernel (see lad_locus.cuh controller()).
 template <int PMAX>
 struct BlockAccess {
+    static constexpr bool kYield = false;  // controller states jump directly (lad_locus.cuh, ACT_YIELD)
     int n, p, lane;
     BlockMem<PMAX> M;
     __device__ __forceinline__ bool leader() const { return threadIdx.x == 0; }

@@ -262,6 +262,7 @@ __device__ __forceinline__ T warp_np_sum(T v, int cnt, int lane)
 // Access policy: the whole warp works on one problem held in WarpShared.
 template <int PMAX, typename T>
 struct WarpAccess {
+    static constexpr bool kYield = false;  // controller states jump directly (lad_locus.cuh, ACT_YIELD)
     int n, p, lane;
     WarpShared<PMAX, T> *W;
     __device__ __forceinline__ bool leader() const { return lane == 0; }

@@ -47,7 +47,7 @@ def warm_radius(beta_prev, status_prev):
 
 
 def solve_lambda_path_batched(X, y, lambdas, cfg: LocusConfig | None = None, *, warm: bool = False,
-                              lambda_floor: float = DEFAULT_LAMBDA_FLOOR, groups: int = 4) -> dict:
+                              lambda_floor: float = DEFAULT_LAMBDA_FLOOR, groups: int = 2) -> dict:
     """Solve every dataset of X (Bd, n, p), y (Bd, n) at every lambda of `lambdas` (L,).
 
     Returns a dict of per-(dataset, lambda) arrays shaped (Bd, L, ...) in the order of

@@ -46,7 +46,7 @@ rules += [("walk", h1 + 1, h2), ("skip", h2 + 1, dd), ("ddot", dd + 1, ac), ("ac
 rules.append(("sparse_step",) + func(W, r"StepState<T> sparse_step\("))
 rules.append(("div",) + func(W, r"__forceinline__ void warp_step\("))
 rules.append(("objective",) + func(W, r"T warp_objective\("))
-d0, d1 = func(W, r"void warp_descent\(")
+d0, d1 = func(W, r"void warp_descent_body\(")
 j0 = find(W, r"int j = j0;", d0)
 ob = find(W, r"const T obj = warp_objective", j0)
 rules += [("dinit", d0, j0 + 1), ("dend", ob + 1, d1), ("dloop", j0 + 2, ob)]
