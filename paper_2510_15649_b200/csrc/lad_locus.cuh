@@ -1061,6 +1061,20 @@ __device__ __forceinline__ void bset(double (&b)[PMAX], int j, double v)
 constexpr double THREAD_MEDIAN_MARGIN = 1e-9;
 
 
+// Rows of the per-lane breakpoint staging column Ls: the n data rows; the lambda breakpoint's
+// constant 0 has a row only for the median guess (LAD_THREAD_CAND), which reads it by index.
+// Without it the config-1 kernel's shared memory is exactly 10 KB per one-warp block, so its 12
+// blocks per SM fit the 132 KB carve-out and leave 124 KB of L1 for the controller state in
+// local memory (164 KB / 92 KB with the extra row).
+// LAD_THREAD_LS = 0: no staging column at all for the rank-sum median (its only reader is the
+// rare exact-order fallback, which then takes the breakpoints from a stack array).
+#ifndef LAD_THREAD_LS
+#define LAD_THREAD_LS 0
+#endif
+constexpr bool thread_ls_v = LAD_THREAD_LS || LAD_THREAD_CAND || !LAD_THREAD_RANK;
+template <int NMAX>
+constexpr int thread_ls_rows = !thread_ls_v ? 0 : NMAX + (LAD_THREAD_CAND ? 1 : 0);
+
 struct MedianPick {
     double t;
     int ik;  // index of the element at the median position
@@ -1071,7 +1085,7 @@ struct MedianPick {
 // ordered by the register sort network, then numpy's cumsum decides
 // (ccd.py:83-90), as in step_dense.
 template <int NMAX, int PMAX>
-__device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double *xc, int lane, double lam)
+__device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double *xc, int lane, double lam, int ls_stride = 32)
 {
     constexpr int NE = NMAX + 1;
     constexpr int XS = PMAX * 32;
@@ -1079,7 +1093,9 @@ __device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double
     int idx[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
-        key[i] = Ls[i * 32 + lane];
+        // Ls: the lane's staging column (stride 32, already offset by the caller when ls_stride == 1:
+        // a stack array); the lambda breakpoint sits at 0
+        key[i] = (i < NMAX || i < thread_ls_rows<NMAX>) ? Ls[ls_stride == 32 ? i * 32 + lane : i] : 0.0;
         idx[i] = i;
     }
     sort_pairs<NE>(key, idx);
@@ -1145,7 +1161,7 @@ __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX],
             const double x = xc[i * XS];
             // np.divide then += b[j] (ccd.py:165-166)
             loc[i] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], x, rc[i * XS]) : div_thread(r[i], x), bj);
-            Ls[i * 32 + lane] = loc[i];
+            if constexpr (thread_ls_v) Ls[i * 32 + lane] = loc[i];
             w[i] = fabs(x);
             wb[i] = 0.0;
             total = dadd(total, w[i]);
@@ -1171,7 +1187,16 @@ __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX],
             t_new = c ? loc[i] : t_new;
             found = found | c;
         }
-        if (!found) t_new = median_by_sort<NMAX, PMAX>(Ls, xc, lane, lam).t;
+        if (!found) {
+            if constexpr (thread_ls_v) {
+                t_new = median_by_sort<NMAX, PMAX>(Ls, xc, lane, lam).t;
+            } else {
+                double tmp[NMAX];
+#pragma unroll
+                for (int i = 0; i < NMAX; ++i) tmp[i] = loc[i];
+                t_new = median_by_sort<NMAX, PMAX>(tmp, xc, lane, lam, 1).t;
+            }
+        }
         if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
         const double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
         const double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, loc[i])); }, [&](int i) { return w[i]; });
@@ -1391,7 +1416,7 @@ template <int NMAX, int PMAX, bool EXACT>
 __host__ __device__ constexpr size_t smem_doubles_per_warp()
 {
     return (size_t)NMAX * PMAX * 32 * (EXACT && LAD_THREAD_RCP ? 2 : 1) +
-           (EXACT && LAD_THREAD_YGLOBAL ? 0 : (size_t)NMAX * 32) + (size_t)(NMAX + 1) * 32 +
+           (EXACT && LAD_THREAD_YGLOBAL ? 0 : (size_t)NMAX * 32) + (size_t)thread_ls_rows<NMAX> * 32 +
            (EXACT && LAD_THREAD_CAND ? (size_t)PMAX * 32 : 0);
 }
 
@@ -1413,21 +1438,31 @@ __host__ __device__ constexpr size_t smem_doubles_per_warp()
 #ifndef LAD_THREAD_MIN_BLOCKS
 #define LAD_THREAD_MIN_BLOCKS 12
 #endif
+// Warps per block of the compile-time-shape kernel.  Each block pays 1 KB of reserved shared
+// memory: with two warps per block the 12 warps of an SM need 6 x (15 + 1) = 96 KB, which fits the
+// 100 KB carve-out (156 KB of L1 for the controller state in local memory) where 12 one-warp
+// blocks need 102 KB and get the 132 KB one.  The warps of a block are independent (no barrier).
+#ifndef LAD_THREAD_WARPS
+#define LAD_THREAD_WARPS 2
+#endif
 template <int NMAX, bool EXACT>
-constexpr int thread_min_blocks = (EXACT && NMAX <= 10) ? LAD_THREAD_MIN_BLOCKS : 1;
+constexpr int thread_warps = (EXACT && NMAX <= 10) ? LAD_THREAD_WARPS : 1;
+template <int NMAX, bool EXACT>
+constexpr int thread_min_blocks =
+    (EXACT && NMAX <= 10) ? (LAD_THREAD_MIN_BLOCKS + LAD_THREAD_WARPS - 1) / LAD_THREAD_WARPS : 1;
 
 template <int NMAX, int PMAX, bool EXACT>
-__global__ void __launch_bounds__(32, thread_min_blocks<NMAX, EXACT>) locus_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32 * thread_warps<NMAX, EXACT>, thread_min_blocks<NMAX, EXACT>) locus_kernel(LocusArgs A)
 {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
     constexpr bool ysh = !(EXACT && LAD_THREAD_YGLOBAL);  // y staged in shared memory
-    double *Xs = smem;
+    double *Xs = smem + (threadIdx.x >> 5) * smem_doubles_per_warp<NMAX, PMAX, EXACT>();  // this warp's region
     double *Ys = ysh ? Xs + NMAX * PMAX * 32 : nullptr;
     double *Ls = Xs + NMAX * PMAX * 32 + (ysh ? NMAX * 32 : 0);
-    double *Tw = Ls + (NMAX + 1) * 32;                                // LAD_THREAD_CAND: PMAX * 32 doubles
+    double *Tw = Ls + thread_ls_rows<NMAX> * 32;                                // LAD_THREAD_CAND: PMAX * 32 doubles
     double *RX = Tw + (EXACT && LAD_THREAD_CAND ? PMAX * 32 : 0);   // LAD_THREAD_RCP: NMAX * PMAX * 32 doubles
-    Ls[NMAX * 32 + lane] = 0.0;  // the lambda breakpoint's location
+    if constexpr (thread_ls_rows<NMAX> > NMAX) Ls[NMAX * 32 + lane] = 0.0;  // the lambda breakpoint's location
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = EXACT ? NMAX : A.n;
     const int p = EXACT ? PMAX : A.p;

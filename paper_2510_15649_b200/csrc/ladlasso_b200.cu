@@ -78,19 +78,23 @@ struct Variant {
     size_t smem;      // dynamic shared memory per block
     int block;        // threads per block
     int slots_per_block;  // independent solvers (seen-list slots) per block
+    bool warp_mapped;     // warp-per-problem kernel (the axis-parallel mode's work items)
+    int carveout_blocks;  // > 0: ask for the smallest shared-memory carve-out that holds this many blocks per SM
 };
 
 template <int N, int P, bool EXACT>
 Variant make_thread_variant()
 {
-    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P, EXACT>() * sizeof(double), 32, 32};
+    constexpr int w = lad::thread_warps<N, EXACT>;
+    return Variant{lad::locus_kernel<N, P, EXACT>, N, P, lad::smem_doubles_per_warp<N, P, EXACT>() * sizeof(double) * w,
+                   32 * w, 32 * w, false, EXACT ? lad::thread_min_blocks<N, EXACT> : 0};
 }
 
 template <int P, int NC, typename T = double>
 Variant make_warp_variant()
 {
     constexpr int wpb = lad::warps_per_block<P, T>;
-    return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, sizeof(lad::WarpShared<P, T>) * wpb, 32 * wpb, wpb};
+    return Variant{lad::locus_warp_kernel<P, NC, T>, 31, P, sizeof(lad::WarpShared<P, T>) * wpb, 32 * wpb, wpb, true, 0};
 }
 
 int g_kernel_policy = LAD_KERNEL_AUTO;
@@ -124,7 +128,7 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
     const bool block_ok = n >= 32 && n <= lad::BLK_NMAX && p <= 8;
     if (block_ok && !(g_kernel_policy == LAD_KERNEL_THREAD && n <= 32)) {  // block per problem (32 <= n <= 1023)
         const int threads = std::min(lad::BLK_THREADS, 32 * ((n + 1 + 31) / 32));
-        v = Variant{lad::locus_block_kernel<8>, lad::BLK_NMAX, 8, lad::block_layout<8>(n, p).total, threads, 1};
+        v = Variant{lad::locus_block_kernel<8>, lad::BLK_NMAX, 8, lad::block_layout<8>(n, p).total, threads, 1, false, 0};
         return true;
     }
     if (thread_exact) v = make_thread_variant<10, 2, true>();
@@ -135,6 +139,7 @@ bool pick_variant(int n, int p, Variant &v, bool f32)
 }
 
 int g_num_sms = 0;
+int g_smem_per_sm = 228 * 1024;  // shared memory per SM (the carve-out preference is a percentage of it)
 std::atomic<uint64_t> g_pool_devices{0};  // devices whose default pool keeps freed scratch mapped
 
 // Per-process, per-device setup: the SM count (grid sizing) and the default
@@ -149,6 +154,9 @@ cudaError_t device_init()
     if (g_num_sms == 0) {
         e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return e;
+        int smem = 0;
+        if (cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) == cudaSuccess && smem > 0)
+            g_smem_per_sm = smem;
     }
     const uint64_t bit = 1ull << (dev & 63);
     if (!(g_pool_devices.load() & bit)) {
@@ -218,6 +226,13 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
 
     CK(device_init());
     if (v.smem > 48 * 1024) CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v.smem));
+    if (v.carveout_blocks > 0) {
+        // the thread kernel keeps its controller state in local memory: every KB of L1 counts, so
+        // ask for the smallest carve-out that still holds its resident blocks (+1 KB reserved each)
+        const size_t need = (size_t)v.carveout_blocks * (v.smem + 1024);
+        const int pct = (int)std::min<size_t>(100, (need * 100 + g_smem_per_sm - 1) / g_smem_per_sm);
+        CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    }
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.block, v.smem));
     if (per_sm < 1) return fail(LAD_E_CUDA, "locus kernel does not fit on an SM (smem %zu)", v.smem);
@@ -228,7 +243,7 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     // tail (scripts/axis_threshold.py: B = 8,192 +11% for config 2 shapes, +5%
     // for config 4; equal at 16,384), despite searching every axis where the
     // serial scan stops after two confirmations.
-    const bool axis_par = g_axis_parallel && mode == lad::MODE_LOCUS && v.block > 32 && prm->outer_axis < 0 &&
+    const bool axis_par = g_axis_parallel && mode == lad::MODE_LOCUS && v.warp_mapped && prm->outer_axis < 0 &&
                           p > 1 && (g_axis_parallel == 2 || B < 2 * max_grid * v.slots_per_block);
     const int64_t items = axis_par ? B * p : B;
     int64_t want = (items + v.slots_per_block - 1) / v.slots_per_block;
