@@ -358,6 +358,7 @@ struct ThreadAccess {
     double *Xs, *Ys;
     double *Tw;  // per axis: sum of the breakpoint weights (|x_ij| and lambda), any order (median guess test)
     double *RX;  // RN(1 / x_ij), same layout as Xs (division by reciprocal), or null
+    float *Sc;   // per axis: 2^30 / (sum of the breakpoint weights), the fixed-point weight scale (rank-sum median), or null
     __device__ __forceinline__ bool leader() const { return true; }
     __device__ __forceinline__ void sync() const {}
     // this slot's curve-point scratch (seen list), null when unused (p <= 2)
@@ -434,6 +435,12 @@ struct ThreadAccess {
                 double s = C.lam;
                 for (int i = 0; i < n; ++i) s += fabs(Xs[(i * PMAX + j) * 32 + lane]);
                 Tw[j * 32 + lane] = s;
+            }
+        if (Sc != nullptr)
+            for (int j = 0; j < p; ++j) {  // any summation order and any rounding of the scale will do (step_dense)
+                double s = C.lam;
+                for (int i = 0; i < n; ++i) s += fabs(Xs[(i * PMAX + j) * 32 + lane]);
+                Sc[j * 32 + lane] = (s > 0.0 && s < 1e300) ? (float)(1073741824.0 / (s * (1.0 + 1e-6))) : 0.0f;
             }
         if (!ok) {
             write_invalid<PMAX>(A, (int64_t)pr, p);
@@ -1008,6 +1015,13 @@ __device__ __noinline__ int controller(Ctl<PMAX> &C, const LocusArgs &A, const A
 #ifndef LAD_THREAD_RANK
 #define LAD_THREAD_RANK 1
 #endif
+// The rank sums in fixed point (weights scaled to 2^30 per total, as in the warp kernel's median
+// test): a pair costs a comparison and two predicated integer adds instead of two FP64 adds and
+// four selects, and the 2^14-unit margin makes an accepted element the reference's (see step_dense).
+#ifndef LAD_THREAD_QRANK
+#define LAD_THREAD_QRANK 1
+#endif
+constexpr bool thread_qrank_v = LAD_THREAD_RANK && LAD_THREAD_QRANK && !LAD_THREAD_CAND;
 // Thread kernel's breakpoint division by a per-problem reciprocal table in
 // shared memory (div_by_rcp: Markstein, bit-identical to r / x), columns with
 // a divisor outside 2^+-450 on the generic path.
@@ -1059,6 +1073,7 @@ __device__ __forceinline__ void bset(double (&b)[PMAX], int j, double v)
 }
 
 constexpr double THREAD_MEDIAN_MARGIN = 1e-9;
+constexpr unsigned MEDIAN_MARGIN_QT = 1u << 14;  // fixed-point rank sums: 2^14 units of 2^-30 of the total
 
 
 // Rows of the per-lane breakpoint staging column Ls: the n data rows; the lambda breakpoint's
@@ -1138,7 +1153,8 @@ __device__ __noinline__ MedianPick median_by_sort(const double *Ls, const double
 // Returns true if the step moved beta_j.
 template <int NMAX, int PMAX>
 __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX], const double *Xs, const double *RX,
-                                           double *Ls, int lane, int j, double lam, double &f_cur, double &sum_abs_b)
+                                           double *Ls, const float *Sc, int lane, int j, double lam, double &f_cur,
+                                           double &sum_abs_b)
 {
     constexpr int NE = NMAX + 1;
     constexpr int XS = PMAX * 32;  // row stride of Xs in doubles
@@ -1146,7 +1162,80 @@ __device__ __forceinline__ void step_dense(double (&r)[NMAX], double (&b)[PMAX],
     const double *rc = RX + j * 32 + lane;
     const double bj = bget(b, j);
     double t_new;
-    if constexpr (LAD_THREAD_RANK) {
+    if constexpr (thread_qrank_v) {
+        // Weighted median by rank sums in fixed point.  qb[i] = weight ordered before element i in
+        // the stable (location, index) order (for q < i, q comes first iff loc_q <= loc_i), summed
+        // over the weights scaled by s ~ 2^30 / total and truncated: every sum of <= NE terms is an
+        // exact integer within NE units below s times the true sum, and so is the total.  Element
+        // m is accepted iff qb + 2^14 < tq / 2 and qb + q_m > tq / 2 + 2^14: then the true sums
+        // clear half the total by ~1.5e-5 * total on both sides, far beyond numpy's cumsum rounding
+        // (NE * 2^-53 * total), so m is numpy's k and not the 1e-12 midpoint tie (ccd.py:83-90).
+        // The scale only has to be the same for every term (a float from the problem's fetch; 0
+        // for a degenerate total, which accepts nothing).  Otherwise (rare) the exact order decides.
+        double loc[NE], w[NE];
+        unsigned wq[NE], qb[NE];
+        const double sc = (double)Sc[j * 32 + lane];
+        unsigned tq = 0u;
+#pragma unroll
+        for (int i = 0; i < NMAX; ++i) {
+            const double x = xc[i * XS];
+            // np.divide then += b[j] (ccd.py:165-166)
+            loc[i] = dadd(LAD_THREAD_RCP ? div_by_rcp(r[i], x, rc[i * XS]) : div_thread(r[i], x), bj);
+            if constexpr (thread_ls_v) Ls[i * 32 + lane] = loc[i];
+            w[i] = fabs(x);
+            wq[i] = __double2uint_rz(dmul(w[i], sc));
+            qb[i] = 0u;
+            tq += wq[i];
+        }
+        loc[NMAX] = 0.0;
+        w[NMAX] = lam;
+        wq[NMAX] = __double2uint_rz(dmul(lam, sc));
+        qb[NMAX] = 0u;
+        tq += wq[NMAX];
+#pragma unroll
+        for (int i = 1; i < NE; ++i)
+#pragma unroll
+            for (int q = 0; q < i; ++q) {
+                // one comparison and two predicated integer adds (written in PTX: the compiler
+                // otherwise selects an addend and adds unconditionally, two instructions more per pair)
+                asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %2, %3;\n\t@p add.u32 %0, %0, %4;\n\t@!p add.u32 %1, %1, %5;\n\t}"
+                    : "+r"(qb[i]), "+r"(qb[q])
+                    : "d"(loc[q]), "d"(loc[i]), "r"(wq[q]), "r"(wq[i]));
+            }
+        const unsigned hq = tq >> 1;
+        const unsigned lo_b = hq >= MEDIAN_MARGIN_QT ? hq - MEDIAN_MARGIN_QT : 0u, hi_b = hq + MEDIAN_MARGIN_QT;
+        bool found = false;
+        t_new = 0.0;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+            const bool c = (qb[i] < lo_b) & (qb[i] + wq[i] > hi_b);
+            t_new = c ? loc[i] : t_new;
+            found = found | c;
+        }
+        if (!found) {
+            if constexpr (thread_ls_v) {
+                t_new = median_by_sort<NMAX, PMAX>(Ls, xc, lane, lam).t;
+            } else {
+                double tmp[NMAX];
+#pragma unroll
+                for (int i = 0; i < NMAX; ++i) tmp[i] = loc[i];
+                t_new = median_by_sort<NMAX, PMAX>(tmp, xc, lane, lam, 1).t;
+            }
+        }
+        if (fabs(dsub(t_new, bj)) <= dmul(1e-14, dadd(1.0, fabs(bj)))) return;  // ccd.py:172
+        const double constant = dmul(lam, dsub(sum_abs_b, fabs(bj)));
+        const double dot = blas_ddot_c<NE>([&](int i) { return fabs(dsub(t_new, loc[i])); }, [&](int i) { return w[i]; });
+        const double v_new = dadd(constant, dot);
+        if (v_new < f_cur) {  // strict accept (ccd.py:187-191)
+            const double delta = dsub(t_new, bj);
+#pragma unroll
+            for (int i = 0; i < NMAX; ++i) r[i] = dsub(r[i], dmul(xc[i * XS], delta));
+            sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
+            bset(b, j, t_new);
+            f_cur = v_new;
+        }
+        return;
+    } else if constexpr (LAD_THREAD_RANK) {
         // Weighted median by rank sums: wb[i] = weight ordered before element i in
         // the stable (location, index) order, one comparison per pair (for j < i, j
         // comes first iff loc_j <= loc_i).  Sums in any order are within NE * 2^-53
@@ -1417,7 +1506,7 @@ __host__ __device__ constexpr size_t smem_doubles_per_warp()
 {
     return (size_t)NMAX * PMAX * 32 * (EXACT && LAD_THREAD_RCP ? 2 : 1) +
            (EXACT && LAD_THREAD_YGLOBAL ? 0 : (size_t)NMAX * 32) + (size_t)thread_ls_rows<NMAX> * 32 +
-           (EXACT && LAD_THREAD_CAND ? (size_t)PMAX * 32 : 0);
+           (EXACT && LAD_THREAD_CAND ? (size_t)PMAX * 32 : 0) + (EXACT && thread_qrank_v ? (size_t)PMAX * 16 : 0);
 }
 
 
@@ -1462,6 +1551,7 @@ __global__ void __launch_bounds__(32 * thread_warps<NMAX, EXACT>, thread_min_blo
     double *Ls = Xs + NMAX * PMAX * 32 + (ysh ? NMAX * 32 : 0);
     double *Tw = Ls + thread_ls_rows<NMAX> * 32;                                // LAD_THREAD_CAND: PMAX * 32 doubles
     double *RX = Tw + (EXACT && LAD_THREAD_CAND ? PMAX * 32 : 0);   // LAD_THREAD_RCP: NMAX * PMAX * 32 doubles
+    float *Sc = reinterpret_cast<float *>(RX + (EXACT && LAD_THREAD_RCP ? NMAX * PMAX * 32 : 0));  // thread_qrank_v: PMAX * 32 floats
     if constexpr (thread_ls_rows<NMAX> > NMAX) Ls[NMAX * 32 + lane] = 0.0;  // the lambda breakpoint's location
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = EXACT ? NMAX : A.n;
@@ -1496,7 +1586,7 @@ __global__ void __launch_bounds__(32 * thread_warps<NMAX, EXACT>, thread_min_blo
         const unsigned ctl_lanes = __ballot_sync(0xffffffffu, alive && need_ctl);
         if (alive && need_ctl) {
             ThreadAccess<NMAX, PMAX> acc{n, p, lane, Xs, Ys, EXACT && LAD_THREAD_CAND ? Tw : nullptr,
-                                         EXACT && LAD_THREAD_RCP ? RX : nullptr};
+                                         EXACT && LAD_THREAD_RCP ? RX : nullptr, EXACT && thread_qrank_v ? Sc : nullptr};
             int act;
             if constexpr (ThreadAccess<NMAX, PMAX>::kYield) {
                 // rounds: every lane still in the controller runs to its next yield point, request or
@@ -1569,7 +1659,7 @@ __global__ void __launch_bounds__(32 * thread_warps<NMAX, EXACT>, thread_min_blo
                 if constexpr (LAD_THREAD_CAND)
                     step_dense_cand<NMAX, PMAX>(r, b, cand, Xs, RX, Ls, Tw, lane, j, lam, f_cur, sum_abs_b);
                 else
-                    step_dense<NMAX, PMAX>(r, b, Xs, RX, Ls, lane, j, lam, f_cur, sum_abs_b);
+                    step_dense<NMAX, PMAX>(r, b, Xs, RX, Ls, Sc, lane, j, lam, f_cur, sum_abs_b);
             }
         }
         if (!dense_step) {

@@ -229,8 +229,16 @@ int run_locus(const void *X, const void *Y, const void *lam, const int64_t *data
     if (v.carveout_blocks > 0) {
         // the thread kernel keeps its controller state in local memory: every KB of L1 counts, so
         // ask for the smallest carve-out that still holds its resident blocks (+1 KB reserved each)
+        // (the preference is a percentage the driver rounds up to a supported size: name the size)
         const size_t need = (size_t)v.carveout_blocks * (v.smem + 1024);
-        const int pct = (int)std::min<size_t>(100, (need * 100 + g_smem_per_sm - 1) / g_smem_per_sm);
+        static const int kCarveKB[] = {0, 8, 16, 32, 64, 100, 132, 164, 196, 228};
+        size_t pick = (size_t)g_smem_per_sm;
+        for (int kb : kCarveKB)
+            if ((size_t)kb * 1024 >= need) {
+                pick = (size_t)kb * 1024;
+                break;
+            }
+        const int pct = (int)std::min<size_t>(100, pick * 100 / (size_t)g_smem_per_sm);
         CK(cudaFuncSetAttribute(v.fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
     }
     int per_sm = 0;
