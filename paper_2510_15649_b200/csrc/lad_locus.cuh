@@ -229,9 +229,15 @@ __device__ double objective_of(const double *Xs, const double *Yp, int ys, int n
             goto L_PC_PR_BEGIN;        \
         }                              \
     } while (0)
+#ifndef LAD_THREAD_YIELD_FINISH  // yield before the evaluator's finish state
+#define LAD_THREAD_YIELD_FINISH 0
+#endif
+#ifndef LAD_THREAD_YIELD_RET     // yield after it, before the probe's caller resumes
+#define LAD_THREAD_YIELD_RET 1
+#endif
 #define PROBE_FINISH()                 \
     do {                               \
-        if constexpr (AC::kYield) {    \
+        if constexpr (AC::kYield && LAD_THREAD_YIELD_FINISH) {    \
             C.pc = PC_PR_FINISH;       \
             return ACT_YIELD;          \
         } else {                       \
@@ -391,7 +397,7 @@ struct ThreadAccess {
         __threadfence();
         return last;
     }
-    __device__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
+    __device__ __forceinline__ int fetch(Ctl<PMAX> &C, const LocusArgs &A) const
     {
         const int div = A.axis_mode == AXIS_SEARCH ? p : 1;
         unsigned long long item = atomicAdd(A.counter, 1ULL);
@@ -481,6 +487,19 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
     double *seen = acc.template seen_base<PMAX>(A, slot);
     for (;;) {
         acc.sync();
+        if constexpr (AC::kYield) {
+            // the states a re-entry usually resumes at, by compare-and-branch: the switch's jump
+            // table costs a dependent constant load and an indirect branch per round
+            int pc = C.pc;
+            asm volatile("" : "+r"(pc));  // opaque: otherwise the compiler folds the chain back into the jump table
+            if (pc == PC_PR_BEGIN) goto L_PC_PR_BEGIN;
+            if (pc == PC_PR_FINISH) goto L_PC_PR_FINISH;
+            if (pc == PC_PR_AFTER_COLD) goto L_PC_PR_AFTER_COLD;
+            if (pc == PC_PR_AFTER_REFINE) goto L_PC_PR_AFTER_REFINE;
+            if (pc == PC_OT_V1) goto L_PC_OT_V1;
+            if (pc == PC_OT_V2) goto L_PC_OT_V2;
+            if (pc == PC_OQ_PROBE) goto L_PC_OQ_PROBE;
+        }
         switch (C.pc) {
         L_PC_FETCH:
         case PC_FETCH: {
@@ -681,7 +700,9 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_OUTER_END);
         }
+        L_PC_OT_V1:
         case PC_OT_V1: C.v1 = C.probe_v; PROBE(C.m2, PC_OT_V2);
+        L_PC_OT_V2:
         case PC_OT_V2: {
             if (C.v1 < C.probe_v) C.hi = C.m2;
             else C.lo = C.m1;
@@ -697,6 +718,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             PROBE(dmul(0.5, dadd(C.lo, C.hi)), PC_OUTER_END);
         }
+        L_PC_OQ_PROBE:
         case PC_OQ_PROBE: {
             double t = dadd(C.lo, dmul(C.h, (double)C.qk));
             if (C.qk == 1 || C.probe_v < C.bv) {
@@ -931,6 +953,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
                                             PC_PR_AFTER_FAST_ONLY);
             ISSUE(jj_ == C.axis ? t : 0.0, C.axis, C.fast_tol, C.fast_sweeps, PC_PR_AFTER_COLD);
         }
+        L_PC_PR_AFTER_COLD:
         case PC_PR_AFTER_COLD: {
             set_point_from_result(acc, C, C.pt, C.probe_t, p);
             if (C.warm_idx >= 0 && p > 2) {
@@ -958,6 +981,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             PROBE_FINISH();
         }
+        L_PC_PR_AFTER_REFINE:
         case PC_PR_AFTER_REFINE: {
             if (C.res_obj < C.pt.value) set_point_from_result(acc, C, C.pt, C.probe_t, p);
             PROBE_FINISH();
@@ -973,7 +997,7 @@ __device__ __forceinline__ int controller_body(Ctl<PMAX> &C, const LocusArgs &A,
             }
             C.probe_v = C.pt.value;
             C.pc = C.ret_pc;  // the probe's caller: the one dynamic transition (through the switch)
-            if constexpr (AC::kYield) return ACT_YIELD;
+            if constexpr (AC::kYield && LAD_THREAD_YIELD_RET) return ACT_YIELD;
             break;
         }
         default:
