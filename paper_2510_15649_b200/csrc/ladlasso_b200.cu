@@ -4,6 +4,7 @@
 // the BASELINE.json shapes (register-resident sort network, fully unrolled
 // reduction trees) and a runtime-shape instantiation for everything else.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -412,6 +413,15 @@ extern "C" int lad_ccd_descend_f32(const float *X, const float *Y, const float *
                      sweep_tolerance, max_sweeps, true);
 }
 
+// problems per chunk of the pipelined host-buffer solve (below).  Config 1, 2^20 problems from pinned
+// host arrays, same box: one launch 56.2 ms, chunks of 2^19 / 2^18 / 2^17 / 2^16: 53.1 / 52.8 / 56.5 / 57.7 ms
+// (smaller chunks lose more to their launch tails than the overlap of the copies wins)
+static const int64_t HOST_CHUNK = [] {
+    const char *v = getenv("LAD_HOST_CHUNK");  // tuning knob (problems per chunk)
+    const long long c = v ? atoll(v) : 0;
+    return (int64_t)(c >= 1024 ? c : (1 << 18));
+}();
+
 template <typename T>
 static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t *data_index, int64_t Bd, int64_t B,
                             int32_t n, int32_t p, const lad_locus_params *prm, const lad_locus_out *out, void *stream,
@@ -450,6 +460,64 @@ static int locus_solve_host(const T *X, const T *Y, const T *lam, const int64_t 
     dout.steps = out->steps ? (int64_t *)take(B * 8) : nullptr;
     int rc = LAD_OK;
     cudaError_t e = cudaSuccess;
+    // Large batches of independent problems (no data_index): the batch is cut into chunks that
+    // alternate between two side streams, so one chunk's copies overlap the other's solve and the
+    // solves fill each other's launch tails.  Results are those of the single launch (problems are
+    // independent); the caller's stream is joined before the call returns.
+    if (!data_index && !brackets && B >= 2 * HOST_CHUNK) {
+        cudaStream_t ss[2] = {nullptr, nullptr};
+        cudaEvent_t ev0 = nullptr, ev[2] = {nullptr, nullptr};
+        e = cudaStreamCreateWithFlags(&ss[0], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ss[1], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ev0, st);  // after the allocation and the caller's earlier work
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamWaitEvent(ss[k], ev0, 0);
+        int64_t c = 0;
+        for (int64_t off = 0; off < B && e == cudaSuccess && rc == LAD_OK; off += HOST_CHUNK, ++c) {
+            const int64_t nb = std::min<int64_t>(HOST_CHUNK, B - off);
+            cudaStream_t sc = ss[c & 1];
+            const size_t xo = (size_t)off * n * p, yo = (size_t)off * n;
+            e = cudaMemcpyAsync(dX + xo, X + xo, (size_t)nb * n * p * es, cudaMemcpyHostToDevice, sc);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(dY + yo, Y + yo, (size_t)nb * n * es, cudaMemcpyHostToDevice, sc);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(dL + off, lam + off, (size_t)nb * es, cudaMemcpyHostToDevice, sc);
+            if (e != cudaSuccess) break;
+            lad_locus_out co = dout;
+            co.beta += (size_t)off * p;
+            co.objective += off;
+            co.iterations += off;
+            co.objective_evals += off;
+            co.converged += off;
+            co.status += off;
+            if (co.descents) co.descents += off;
+            if (co.steps) co.steps += off;
+            if constexpr (sizeof(T) == 4) rc = lad_locus_solve_f32(dX + xo, dY + yo, dL + off, nullptr, nb, nb, n, p, prm, &co, sc);
+            else rc = lad_locus_solve_f64(dX + xo, dY + yo, dL + off, nullptr, nb, nb, n, p, prm, &co, sc);
+            if (rc != LAD_OK) break;
+            struct { void *h; const void *d; size_t w; } cp[] = {
+                {out->beta, dout.beta, (size_t)p * 8}, {out->objective, dout.objective, 8}, {out->iterations, dout.iterations, 4},
+                {out->objective_evals, dout.objective_evals, 4}, {out->converged, dout.converged, 1},
+                {out->status, dout.status, 1}, {out->descents, dout.descents, 4}, {out->steps, dout.steps, 8}};
+            for (auto &q : cp)
+                if (q.h && q.d && e == cudaSuccess)
+                    e = cudaMemcpyAsync((char *)q.h + (size_t)off * q.w, (const char *)q.d + (size_t)off * q.w,
+                                        (size_t)nb * q.w, cudaMemcpyDeviceToHost, sc);
+        }
+        for (int k = 0; k < 2; ++k)  // join the side streams into the caller's (also on an error: nothing may outlive d)
+            if (ss[k] && ev[k] && cudaEventRecord(ev[k], ss[k]) == cudaSuccess) cudaStreamWaitEvent(st, ev[k], 0);
+        cudaFreeAsync(d, st);
+        cudaError_t se = cudaStreamSynchronize(st);
+        for (int k = 0; k < 2; ++k) {
+            if (ss[k]) cudaStreamSynchronize(ss[k]);
+            if (ev[k]) cudaEventDestroy(ev[k]);
+            if (ss[k]) cudaStreamDestroy(ss[k]);
+        }
+        if (ev0) cudaEventDestroy(ev0);
+        if (e != cudaSuccess) return fail(LAD_E_CUDA, "host solve (chunked): %s", cudaGetErrorString(e));
+        if (rc != LAD_OK) return rc;
+        if (se != cudaSuccess) return fail(LAD_E_CUDA, "host solve (chunked): %s", cudaGetErrorString(se));
+        return LAD_OK;
+    }
     if (e == cudaSuccess) e = cudaMemcpyAsync(dX, X, bx, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dY, Y, by, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(dL, lam, bl, cudaMemcpyHostToDevice, st);

@@ -152,3 +152,22 @@ def test_brute_chunked_path_beyond_65535_problems(oracle):
     for i in (0, 65534, 65535, 65536, B - 1):
         ob, oo, on = oracle.solve_brute(X[i], Y[i], float(L[i]))
         assert float(bo[i]) == oo and np.array_equal(np.asarray(bb[i]), ob) and int(bv[i]) == on, i
+
+
+def test_large_host_batch_pipelined_equals_device_solve(oracle):
+    """Host arrays of >= 2^19 independent problems take the chunked two-stream path of
+    lad_locus_solve_host_f64 (copies overlapping solves); its results equal the device-tensor solve
+    of the same problems bit for bit, including a ragged last chunk, and the oracle on a sample."""
+    from paper_2510_15649_b200 import configgen as G
+
+    B = (1 << 19) + 12345
+    X, Y, L = G.generate(1, B, seed=15650, first=4242)
+    dev = lad.solve_locus_batched(X, Y, L)
+    Xh, Yh, Lh = (t.cpu().numpy() for t in (X, Y, L))
+    host = lad.solve_locus_batched(Xh, Yh, Lh)
+    for f in ("beta", "objective", "iterations", "objective_evals", "converged", "status", "descents", "steps"):
+        assert np.array_equal(np.asarray(getattr(host, f)), getattr(dev, f).cpu().numpy()), f
+    idx = np.concatenate([np.arange(0, 64), np.arange((1 << 18) - 32, (1 << 18) + 32), np.arange(B - 64, B)])
+    o = oracle.solve_locus_batch(Xh[idx], Yh[idx], Lh[idx], nthreads=4)
+    assert np.array_equal(np.asarray(host.objective)[idx], o["objective"])
+    assert np.array_equal(np.asarray(host.beta)[idx], o["beta"])
