@@ -379,7 +379,7 @@ def ncu_lookup(key, solves_per_launch, units, elapsed, clocks, dev, unit):
         return None, None
     traffic = tr["bytes_per_solve"] * solves_per_launch if tr.get("bytes_per_solve") is not None else None
     issue = None
-    ipu = tr.get("warp_instr_per_coord_step") if unit == "coordinate step" else tr.get("warp_instr_per_unit")
+    ipu = tr.get("warp_instr_per_unit") or tr.get("warp_instr_per_coord_step")
     if ipu and clocks.get("sm_mhz") and elapsed > 0:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         peak_issue = 4 * sms * clocks["sm_mhz"] * 1e6  # one warp instruction per SMSP per cycle
@@ -455,7 +455,7 @@ def run_aux(a, world, rank, local):
         barrier()
         # a step here is a few ms of GPU time, about what the host needs to enqueue it: a short spin
         # kernel first lets the host run ahead, so the events time the GPU and not the enqueue gaps
-        if hasattr(torch.cuda, "_sleep"):
+        if hasattr(torch.cuda, "_sleep") and not os.environ.get("LAD_BENCH_NO_SPIN"):
             torch.cuda._sleep(200_000_000)
         for k in range(a.steps):
             flush.zero_()

@@ -446,7 +446,10 @@ struct ThreadAccess {
             for (int j = 0; j < p; ++j) {  // any summation order and any rounding of the scale will do (step_dense)
                 double s = C.lam;
                 for (int i = 0; i < n; ++i) s += fabs(Xs[(i * PMAX + j) * 32 + lane]);
-                Sc[j * 32 + lane] = (s > 0.0 && s < 1e300) ? (float)(1073741824.0 / (s * (1.0 + 1e-6))) : 0.0f;
+                // (a total so small or large that the binary32 scale leaves its finite range accepts
+                // nothing: every step of that axis then takes the exact order)
+                const float scf = (float)(1073741824.0 / (s * (1.0 + 1e-6)));
+                Sc[j * 32 + lane] = (s > 0.0 && s < 1e300 && scf > 0.0f && scf < 3.0e38f) ? scf : 0.0f;
             }
         if (!ok) {
             write_invalid<PMAX>(A, (int64_t)pr, p);

@@ -216,7 +216,7 @@ struct BlockAccess {
             for (int e = tid; e <= n; e += (int)blockDim.x) s += e < n ? fabs(M.X[e * p + j]) : lam_eff;
             const double tot = block_sum_d(s, H->redd);
             const double scale = 1073741824.0 / (tot * (1.0 + 1e-9));
-            const bool good = tot > 0.0 && tot < 1e300;
+            const bool good = tot > 0.0 && tot < 1e300 && scale < 1e300;  // a finite scale keeps every weight below 2^30
             unsigned qs = 0;
             for (int e = tid; e <= n; e += (int)blockDim.x)
                 qs += good ? __double2uint_rz((e < n ? fabs(M.X[e * p + j]) : lam_eff) * scale) : 0u;

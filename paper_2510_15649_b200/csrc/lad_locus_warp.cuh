@@ -387,7 +387,8 @@ struct WarpAccess {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(FULLMASK, tot, off);
             const double scale = 1073741824.0 / (tot * (1.0 + 1e-9));
-            const unsigned q = (tot > 0.0 && tot < 1e300) ? __double2uint_rz(wd * scale) : 0u;
+            // (a finite scale keeps every q below 2^30; a total below ~6e-300 would overflow it)
+            const unsigned q = (tot > 0.0 && tot < 1e300 && scale < 1e300) ? __double2uint_rz(wd * scale) : 0u;
             W->wq[j][lane] = q;
             const unsigned sq = __reduce_add_sync(FULLMASK, q);
             if (lane == 0) {

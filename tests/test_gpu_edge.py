@@ -171,3 +171,21 @@ def test_large_host_batch_pipelined_equals_device_solve(oracle):
     o = oracle.solve_locus_batch(Xh[idx], Yh[idx], Lh[idx], nthreads=4)
     assert np.array_equal(np.asarray(host.objective)[idx], o["objective"])
     assert np.array_equal(np.asarray(host.beta)[idx], o["beta"])
+
+
+@pytest.mark.parametrize("shape", [(10, 2), (30, 5), (40, 3)])
+def test_tiny_weight_totals_with_a_lowered_lambda_floor(oracle, shape):
+    """Weights so small that the fixed-point scale 2^30 / total would overflow (possible only with a
+    lambda_floor far below the default): the median tests must accept nothing there and the exact
+    order decides, on the thread, warp and block kernels alike."""
+    n, p = shape
+    rng = np.random.default_rng(31)
+    X = rng.standard_normal((24, n, p)) * 1e-304
+    Y = rng.standard_normal((24, n)) * 1e-304
+    L = np.full(24, 1e-306)
+    o = oracle.solve_locus_batch(X, Y, L, lambda_floor=1e-310, nthreads=4)
+    r = lad.solve_locus_batched(X, Y, L, lambda_floor=1e-310)
+    assert np.array_equal(np.asarray(r.status), o["status"])
+    assert np.array_equal(np.asarray(r.objective), o["objective"])
+    assert np.array_equal(np.asarray(r.beta), o["beta"])
+    assert np.array_equal(np.asarray(r.steps), o["steps"])
