@@ -59,8 +59,11 @@ constexpr int warps_per_block = (PMAX <= 5 || (sizeof(T) == 4 && !LAD_WARP_F32_W
 // reciprocal table (binary32, or binary64 with p <= 5).
 // (For binary64 p = 8 the table costs more than it saves: 2 KB more shared
 // memory per warp, config 4 -13% in a same-box A/B.)
+#ifndef LAD_WARP_FASTDIV8  // the reciprocal table for binary64 p = 8 too
+#define LAD_WARP_FASTDIV8 0
+#endif
 template <int PMAX, typename T>
-constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5;
+constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5 || LAD_WARP_FASTDIV8;
 
 // Pad rows as data (with the reciprocal table): row n of X holds lambda and
 // rows > n hold 0, and the pad lanes' residual stays 1, so every lane's
@@ -133,12 +136,18 @@ constexpr bool padx_v = LAD_WARP_PADX && fast_div_v<PMAX, T>;
 #define LAD_WARP_HQ_LDS 0
 #endif
 
+// Row stride of the per-warp X (and 1/X) copy in elements: p | 1.  Lane i reads x_ij at i * xs + j;
+// with an even stride (p = 8: 16 words) lanes two apart hit the same bank pair, a 16-way conflict
+// on the step's x_ij load and on every row product of the residual init and the objective.
+template <int PMAX>
+constexpr int xs_v = PMAX | 1;
+
 template <int PMAX, typename T>
 struct WarpShared {
     using T2 = typename vec2_of<T>::type;
     Ctl<PMAX> C;
-    T X[32 * PMAX];  // row-major [i * p + j]
-    T RX[fast_div_v<PMAX, T> ? 32 * PMAX : 1];  // RN(1 / x), same layout; 1 for pad lanes
+    T X[32 * xs_v<PMAX>];  // row-major [i * xs + j], xs = p | 1: an odd row stride keeps lane i's row off lane i'+-k's banks
+    T RX[fast_div_v<PMAX, T> ? 32 * xs_v<PMAX> : 1];  // RN(1 / x), same layout; 1 for pad lanes
     T Y[32];
     T B[PMAX];       // beta of the running descent (warp-uniform)
     T sa[32], sw[32], sz[32];
@@ -149,7 +158,7 @@ struct WarpShared {
     unsigned halfq[PMAX];   // per axis: (sum of wq) / 2
     uint2 hqb[PMAX];        // per axis: (halfq - margin (0 if below), halfq + margin)
     double *seen;           // this slot's seen-list scratch (null when unused), set at kernel start
-    alignas(16) T pp[32];   // ddot lane-tree products, lane l's four at [4 l, 4 l + 4) (n1 = 16) / [8 l, 8 l + 8)
+    alignas(16) T pp[LAD_WARP_DDOT_SMEM ? 32 : 2];  // ddot lane-tree products (LAD_WARP_DDOT_SMEM), lane l's four at [4 l, 4 l + 4) (n1 = 16) / [8 l, 8 l + 8)
 };
 
 // margin of the fixed-point median test, in units of 2^-30 of the total weight
@@ -265,6 +274,7 @@ struct WarpAccess {
     static constexpr bool kYield = false;  // controller states jump directly (lad_locus.cuh, ACT_YIELD)
     int n, p, lane;
     WarpShared<PMAX, T> *W;
+    int xs;  // row stride of W->X / W->RX (p | 1)
     __device__ __forceinline__ bool leader() const { return lane == 0; }
     __device__ __forceinline__ void sync() const { __syncwarp(); }
     // the slot's seen list, computed once per kernel (WarpShared::seen)
@@ -354,16 +364,20 @@ struct WarpAccess {
         uint32_t mask = 0;
         for (int e = lane; e < n * p; e += 32) {
             T v = xg[e];
-            W->X[e] = v;
+            const int i = e / p, j = e - i * p;
+            W->X[i * xs + j] = v;
             ok = ok && isfinite(v);
-            if (v == T(0)) mask |= 1u << (e % p);
+            if (v == T(0)) mask |= 1u << j;
             if constexpr (fast_div_v<PMAX, T>) {
-                W->RX[e] = rcp_rn(v);
-                if (!div_operand_safe(v)) mask |= 1u << (e % p);  // column takes the generic path
+                W->RX[i * xs + j] = rcp_rn(v);
+                if (!div_operand_safe(v)) mask |= 1u << j;  // column takes the generic path
             }
         }
         if constexpr (fast_div_v<PMAX, T>)
-            for (int e = n * p + lane; e < 32 * p; e += 32) W->RX[e] = T(1);
+            for (int e = n * p + lane; e < 32 * p; e += 32) {
+                const int i = e / p, j = e - i * p;
+                W->RX[i * xs + j] = T(1);
+            }
         for (int i = lane; i < n; i += 32) {
             T v = yg[i];
             W->Y[i] = v;
@@ -377,12 +391,15 @@ struct WarpAccess {
         ok = ok && isfinite(lraw) && lraw >= 0.0;
         const double lam_eff = lraw > A.prm.lambda_floor ? lraw : A.prm.lambda_floor;
         if constexpr (padx_v<PMAX, T>)  // row n: the lambda breakpoint's weight; rows > n: weight 0
-            for (int e = n * p + lane; e < 32 * p; e += 32) W->X[e] = e < (n + 1) * p ? T(lam_eff) : T(0);
+            for (int e = n * p + lane; e < 32 * p; e += 32) {
+                const int i = e / p, j = e - i * p;
+                W->X[i * xs + j] = i == n ? T(lam_eff) : T(0);
+            }
         __syncwarp();
         // fixed-point breakpoint weights of each axis (median fast path): any
         // summation order will do, the test keeps a margin of 2^14 units
         for (int j = 0; j < p; ++j) {
-            const double wd = lane < n ? (double)fabs(W->X[lane * p + j]) : (lane == n ? (double)T(lam_eff) : 0.0);
+            const double wd = lane < n ? (double)fabs(W->X[lane * xs + j]) : (lane == n ? (double)T(lam_eff) : 0.0);
             double tot = wd;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(FULLMASK, tot, off);
@@ -413,7 +430,7 @@ struct WarpAccess {
     {
         if (p == 1) return (double)np_sum(n, [&](int i) { return fabs(W->X[i]); });
         T s = T(0);
-        for (int i = 0; i < n; ++i) s = dadd(s, fabs(W->X[i * p + j]));
+        for (int i = 0; i < n; ++i) s = dadd(s, fabs(W->X[i * xs + j]));
         return (double)s;
     }
     __device__ double y_absmax(const double *) const
@@ -850,11 +867,11 @@ __device__ __forceinline__ void warp_step(WarpShared<PMAX, T> *W, int lane, uint
 }
 
 template <int PMAX, typename T>
-__device__ __forceinline__ T warp_objective(WarpShared<PMAX, T> *W, int lane, int n, int p, T lam)
+__device__ __forceinline__ T warp_objective(WarpShared<PMAX, T> *W, int lane, int n, int p, int xs, T lam)
 {
     T v = T(0);
     if (lane < n) {
-        T g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * p + q]; }, [&](int q) { return W->B[q]; });
+        T g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * xs + q]; }, [&](int q) { return W->B[q]; });
         v = fabs(dsub(W->Y[lane], g));
     }
     T rs = warp_np_sum(v, n, lane);
@@ -883,6 +900,7 @@ __device__ __forceinline__ void warp_descent_body(WarpShared<PMAX, T> *W, Ctl<PM
 {
     const int n = NC > 0 ? NC : n_rt;
     const int p = NC > 0 ? PMAX : p_rt;
+    const int xs = p | 1;  // row stride of W->X (xs_v)
     const int frozen = C.req_frozen;
     const double tol = C.req_tol;
     const int max_sweeps = C.req_sweeps;
@@ -892,11 +910,11 @@ __device__ __forceinline__ void warp_descent_body(WarpShared<PMAX, T> *W, Ctl<PM
     __syncwarp();
     T r = padx_v<PMAX, T> ? T(1) : T(0);  // pad lanes (padx: a safe dividend that never changes)
     if (lane < n) {
-        T g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * p + q]; }, [&](int q) { return W->B[q]; });
+        T g = gemv_row(p, lane, n, [&](int q) { return W->X[lane * xs + q]; }, [&](int q) { return W->B[q]; });
         r = dsub(W->Y[lane], g);
     }
-    const T *xrow = W->X + lane * p;
-    const T *yrow = fast_div_v<PMAX, T> ? W->RX + lane * p : nullptr;
+    const T *xrow = W->X + lane * xs;
+    const T *yrow = fast_div_v<PMAX, T> ? W->RX + lane * xs : nullptr;
     const T sb = np_sum(p, [&](int q) { return fabs(W->B[q]); });
     T f_cur = dadd(warp_np_sum(fabs(r), n, lane), dmul(lam, sb));
     T f_sweep_start = f_cur, sum_abs_b = sb;
@@ -972,7 +990,7 @@ __device__ __forceinline__ void warp_descent_body(WarpShared<PMAX, T> *W, Ctl<PM
         }
     }
     __syncwarp();
-    const T obj = warp_objective<PMAX, T>(W, lane, n, p, lam);
+    const T obj = warp_objective<PMAX, T>(W, lane, n, p, xs, lam);
     const int D = C.D;
     const long long S = C.S;
     __syncwarp();
@@ -1006,7 +1024,7 @@ __global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS
     WarpShared<PMAX, T> *W = &WS[wib];
     const int n = NC > 0 ? NC : A.n, p = NC > 0 ? PMAX : A.p;
     const int slot = blockIdx.x * warps_per_block<PMAX, T> + wib;
-    WarpAccess<PMAX, T> acc{n, p, lane, W};
+    WarpAccess<PMAX, T> acc{n, p, lane, W, p | 1};
     const uint32_t inv_mask = bitonic_inv_mask(lane);
     Ctl<PMAX> &C = W->C;
     if (lane < PMAX) W->cand[lane] = 0;
