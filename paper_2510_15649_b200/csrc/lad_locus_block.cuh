@@ -66,7 +66,7 @@ __host__ __device__ inline BlockLayout block_layout(int n, int p)
         o = (o + bytes + 15) & ~(size_t)15;
         return r;
     };
-    L.off_X = take((size_t)n * p * 8);
+    L.off_X = take((size_t)n * (p | 1) * 8);  // row stride p | 1: thread i's row stays off its neighbours' banks
     L.off_Y = take((size_t)n * 8);
     L.off_loc = take((size_t)P2 * 8);
     L.off_w = take((size_t)(n + 1) * 8);
@@ -86,6 +86,7 @@ struct BlockMem {
     int *si, *pos;
     double2 *aw;
     int P2;
+    int xs;  // row stride of X in doubles (p | 1)
 };
 
 __device__ __forceinline__ unsigned block_sum_u2(unsigned a, unsigned b, unsigned (*red)[BLK_WARPS], unsigned &sb)
@@ -196,9 +197,10 @@ struct BlockAccess {
         unsigned mask = 0;
         for (int e = tid; e < n * p; e += (int)blockDim.x) {
             const double v = xg[e];
-            M.X[e] = v;
+            const int i = e / p, j = e - i * p;
+            M.X[i * M.xs + j] = v;
             ok = ok && isfinite(v);
-            if (v == 0.0) mask |= 1u << (e % p);
+            if (v == 0.0) mask |= 1u << j;
         }
         for (int i = tid; i < n; i += (int)blockDim.x) {
             const double v = yg[i];
@@ -213,13 +215,13 @@ struct BlockAccess {
         // fixed-point weights per axis for the median test (any summation order will do)
         for (int j = 0; j < p; ++j) {
             double s = 0.0;
-            for (int e = tid; e <= n; e += (int)blockDim.x) s += e < n ? fabs(M.X[e * p + j]) : lam_eff;
+            for (int e = tid; e <= n; e += (int)blockDim.x) s += e < n ? fabs(M.X[e * M.xs + j]) : lam_eff;
             const double tot = block_sum_d(s, H->redd);
             const double scale = 1073741824.0 / (tot * (1.0 + 1e-9));
             const bool good = tot > 0.0 && tot < 1e300 && scale < 1e300;  // a finite scale keeps every weight below 2^30
             unsigned qs = 0;
             for (int e = tid; e <= n; e += (int)blockDim.x)
-                qs += good ? __double2uint_rz((e < n ? fabs(M.X[e * p + j]) : lam_eff) * scale) : 0u;
+                qs += good ? __double2uint_rz((e < n ? fabs(M.X[e * M.xs + j]) : lam_eff) * scale) : 0u;
             unsigned dummy;
             const unsigned sq = block_sum_u2(qs, 0u, H->redu, dummy);
             if (tid == 0) {
@@ -243,7 +245,7 @@ struct BlockAccess {
     {
         if (p == 1) return np_sum_rec(0, n, [&](int i) { return fabs(M.X[i]); });  // contiguous column: pairwise
         double s = 0.0;
-        for (int i = 0; i < n; ++i) s = dadd(s, fabs(M.X[i * p + j]));
+        for (int i = 0; i < n; ++i) s = dadd(s, fabs(M.X[i * M.xs + j]));
         return s;
     }
     __device__ double y_absmax(const double *) const
@@ -349,7 +351,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         for (int q = 0; q < BLK_EPT; ++q) {
             const int e = tid + q * (int)blockDim.x;
             if (e < n) {
-                const double x = M.X[e * p + j];
+                const double x = M.X[e * M.xs + j];
                 M.loc[e] = dadd(ddiv_zero_fast(r[q], x), bj);
                 M.w[e] = fabs(x);
             } else if (e == n) {
@@ -363,7 +365,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
 #pragma unroll
         for (int q = 0; q < BLK_EPT; ++q) {
             const int i = tid * BLK_EPT + q;  // contiguous rows per thread for the scan
-            flags[q] = (i < n && M.X[i * p + j] != 0.0) ? 1 : 0;
+            flags[q] = (i < n && M.X[i * M.xs + j] != 0.0) ? 1 : 0;
             nnz += flags[q];
         }
         int incl = nnz;
@@ -394,7 +396,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
         for (int q = 0; q < BLK_EPT; ++q) {
             const int i = tid * BLK_EPT + q;
             if (i < n) {
-                const double x = M.X[i * p + j];
+                const double x = M.X[i * M.xs + j];
                 if (flags[q]) {
                     M.loc[pnz] = ddiv(dadd(M.tmp[i], dmul(x, bj)), x);
                     M.w[pnz] = fabs(x);
@@ -625,7 +627,7 @@ __device__ void block_step(const BlockMem<PMAX> &M, int n, int p, int j, double 
 #pragma unroll
         for (int q = 0; q < BLK_EPT; ++q) {
             const int i = tid + q * (int)blockDim.x;
-            if (i < n) r[q] = dsub(r[q], dmul(M.X[i * p + j], delta));
+            if (i < n) r[q] = dsub(r[q], dmul(M.X[i * M.xs + j], delta));
         }
         sum_abs_b = dadd(sum_abs_b, dsub(fabs(t_new), fabs(bj)));
         f_cur = v_new;
@@ -640,7 +642,7 @@ __device__ double block_objective(const BlockMem<PMAX> &M, int n, int p, double 
 {
     BlockHead<PMAX> *H = M.H;
     for (int i = threadIdx.x; i < n; i += (int)blockDim.x) {
-        const double g = gemv_row(p, i, n, [&](int q) { return M.X[i * p + q]; }, [&](int q) { return H->B[q]; });
+        const double g = gemv_row(p, i, n, [&](int q) { return M.X[i * M.xs + q]; }, [&](int q) { return H->B[q]; });
         M.tmp[i] = fabs(dsub(M.Y[i], g));
     }
     __syncthreads();
@@ -672,7 +674,7 @@ __device__ void block_descent(const BlockMem<PMAX> &M, Ctl<PMAX> &C, int n, int 
         const int i = tid + q * (int)blockDim.x;
         r[q] = 0.0;
         if (i < n) {
-            const double g = gemv_row(p, i, n, [&](int c) { return M.X[i * p + c]; }, [&](int c) { return H->B[c]; });
+            const double g = gemv_row(p, i, n, [&](int c) { return M.X[i * M.xs + c]; }, [&](int c) { return H->B[c]; });
             r[q] = dsub(M.Y[i], g);
             M.tmp[i] = fabs(r[q]);
         }
@@ -746,6 +748,7 @@ __global__ void __launch_bounds__(BLK_THREADS) locus_block_kernel(LocusArgs A)
     M.tmp = reinterpret_cast<double *>(blk_smem + L.off_tmp);
     M.pos = reinterpret_cast<int *>(blk_smem + L.off_pos);
     M.P2 = L.P2;
+    M.xs = p | 1;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     Ctl<PMAX> &C = M.H->C[wp];
     if (threadIdx.x < PMAX) {
