@@ -29,38 +29,47 @@
 namespace lad {
 
 constexpr unsigned FULLMASK = 0xffffffffu;
-// Launch shape, 4 blocks per SM: 8 warps per block (32 warps/SM, 64 registers),
-// except binary64 p = 8 with 7 (28 warps/SM, 72 registers).  Same-box A/B: 32
-// warps are +3% for config 2, +3.4% for config 4 in fp32 and -2% for config 4
-// in fp64 (whose longer step body spills less at 72 registers); 36 warps at 56
-// registers: -3% for config 2.
+// Launch shape: 4 blocks per SM of 8 warps (32 warps/SM, 64 registers), except
+// binary64 p = 8: 5 blocks of 5 warps (25 warps/SM, 72 registers), the most that
+// fit with its reciprocal table in shared memory (8.5 KB per warp).  Same-box
+// A/B: 32 warps are +3% for config 2, +3.4% for config 4 in fp32; config 4 in
+// fp64 (its longer step body spills less at 72 registers): 8 x 4 at 64 registers
+// -6% against 7 x 4 at 72; with the table 6 x 4 +2% and 5 x 5 +4% against 7 x 4
+// without it; 5 x 6 without the table -7.5%.  36 warps at 56 registers: -3% for
+// config 2.
 #ifndef LAD_WARP_WARPS_NARROW
 #define LAD_WARP_WARPS_NARROW 8
 #endif
 #ifndef LAD_WARP_WARPS_WIDE
-#define LAD_WARP_WARPS_WIDE 7
+#define LAD_WARP_WARPS_WIDE 5
 #endif
-#ifndef LAD_WARP_F32_WIDE  // binary32 p = 8 with the binary64 p = 8 shape (7 warps, 72 registers)
+#ifndef LAD_WARP_F32_WIDE  // binary32 p = 8 with the binary64 p = 8 shape (72 registers)
 #define LAD_WARP_F32_WIDE 0
 #endif
 #ifndef LAD_WARP_MIN_BLOCKS
 #define LAD_WARP_MIN_BLOCKS 4
 #endif
 constexpr int WARP_MIN_BLOCKS = LAD_WARP_MIN_BLOCKS;
+#ifndef LAD_WARP_MIN_BLOCKS_WIDE  // binary64 p = 8
+#define LAD_WARP_MIN_BLOCKS_WIDE 5
+#endif
 template <int PMAX, typename T>
 constexpr int warps_per_block = (PMAX <= 5 || (sizeof(T) == 4 && !LAD_WARP_F32_WIDE)) ? LAD_WARP_WARPS_NARROW
                                                                                     : LAD_WARP_WARPS_WIDE;
+template <int PMAX, typename T>
+constexpr int warp_min_blocks = (PMAX <= 5 || (sizeof(T) == 4 && !LAD_WARP_F32_WIDE)) ? LAD_WARP_MIN_BLOCKS
+                                                                                    : LAD_WARP_MIN_BLOCKS_WIDE;
 
 // Division by a precomputed reciprocal: q = RN(r * y), then two corrections
 // q += RN(r - q * x) * y with y = RN(1 / x).  The first makes q faithful, the
 // second is then correctly rounded (Markstein's theorem), so q == r / x in
 // round-to-nearest whenever nothing under- or overflows: |r| and |x| within
 // 2^+-450 (binary64) or 2^+-50 (binary32).  Used where shared memory holds the
-// reciprocal table (binary32, or binary64 with p <= 5).
-// (For binary64 p = 8 the table costs more than it saves: 2 KB more shared
-// memory per warp, config 4 -13% in a same-box A/B.)
+// reciprocal table.  (For binary64 p = 8 the table lost 13% while the X copy's
+// even row stride put a 16-way bank conflict on every x_ij and 1/x_ij load;
+// with the odd stride (xs_v) and a launch shape that fits it, it wins 4%.)
 #ifndef LAD_WARP_FASTDIV8  // the reciprocal table for binary64 p = 8 too
-#define LAD_WARP_FASTDIV8 0
+#define LAD_WARP_FASTDIV8 1
 #endif
 template <int PMAX, typename T>
 constexpr bool fast_div_v = sizeof(T) == 4 || PMAX <= 5 || LAD_WARP_FASTDIV8;
@@ -1015,7 +1024,7 @@ __device__ __noinline__ void warp_descent(WarpShared<PMAX, T> *W, Ctl<PMAX> &C, 
 
 // PMAX: beta capacity; NC > 0 specialises the row count (and p == PMAX).
 template <int PMAX, int NC, typename T>
-__global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, WARP_MIN_BLOCKS) locus_warp_kernel(LocusArgs A)
+__global__ void __launch_bounds__(32 * warps_per_block<PMAX, T>, warp_min_blocks<PMAX, T>) locus_warp_kernel(LocusArgs A)
 {
     extern __shared__ __align__(16) unsigned char warp_smem[];  // warps_per_block x WarpShared
     WarpShared<PMAX, T> *WS = reinterpret_cast<WarpShared<PMAX, T> *>(warp_smem);
